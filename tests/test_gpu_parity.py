@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Integer work, so the bar is bit-exact everywhere: the ordered list (MATERIALIZE), the count
+(COUNT) and the 64-bit order-sensitive hash (HASH).  Inputs come from fzinputs (seeded or the
+fixed BASELINE configs); every expected value comes from oracle/ or from a cited golden file.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import parse_gens, read_golden_csv
+from fzinputs import (C1_GENS, C1_MAX_N, C1_T, C2, C3_GENS, C3_N, C4, TABLE1_ROWS, random_instance,
+                      random_instance_mid, table1_gens)
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2407_20474_b200 import fz
+
+
+def _np(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _check_materialize(memo, n, corc, g, shards=(1,)):
+    want, cnt, h = corc.enumerate(n, g, use_o2=True)
+    for ns in shards:
+        parts, hs, tot = [], 0, 0
+        for s in range(ns):
+            out, rows, _ = fz.enumerate(memo, n, "materialize", shard=s, nshards=ns)
+            parts.append(_np(out)[:rows])
+            tot += rows
+            _, hr, hh = fz.enumerate(memo, n, "hash", shard=s, nshards=ns)
+            hs = (hs + hh) % (1 << 64)
+        got = np.concatenate(parts) if parts else np.zeros((0, len(g)), np.uint32)
+        assert tot == cnt, (g, n, ns)
+        assert np.array_equal(got.reshape(-1, len(g)), want.reshape(-1, len(g))), (g, n, ns)
+        assert hs == h, (g, n, ns)
+        crow = 0
+        for s in range(ns):
+            _, cr, _ = fz.enumerate(memo, n, "count", shard=s, nshards=ns)
+            crow += cr
+        assert crow == cnt
+
+
+# ----------------------------------------------------------------- memo (K1-K3)
+MEMO_CASES = [((9, 20), 25), ((9, 20), 1001), ((17, 19), 30233), ((41, 43), 17351), ((38, 40), 15001),
+              ((38, 40, 41, 42), 3001), ((3, 5, 8), 500), ((1, 1, 2), 200), ((7,), 300), ((4, 6, 10, 4), 400)]
+
+
+@pytest.mark.parametrize("tail,top", MEMO_CASES, ids=lambda x: str(x))
+def test_memo_rows_vs_alg2(tail, top, corc):
+    """K1-K3 memo == Alg 2 over the tail generators, row by row."""
+    g = (5,) + tuple(tail)          # a leading generator, the memo is over the last t = len(tail)
+    t = len(tail)
+    memo = fz.memo_build(g, t, top)
+    rows, off, S = memo.views()
+    want_rows, want_off = corc.memo_alg2(tail, top)
+    assert np.array_equal(off.cpu().numpy().astype(np.uint64), want_off)
+    assert memo.info["entries"] == len(want_rows)
+    if len(want_rows):
+        assert np.array_equal(_np(rows).reshape(-1, t), want_rows)
+    # count tables: S_i = GF table of g_i..g_d
+    Sh = S.cpu().numpy().astype(np.uint64)
+    for i in range(len(g)):
+        assert np.array_equal(Sh[i], corc.gf_table(top - 1, g[i:])), i
+    assert np.array_equal(Sh[len(g)], (np.arange(top) == 0).astype(np.uint64))
+
+
+@pytest.mark.parametrize("kat", [k for k in read_golden_csv("memo_kats.csv") if k["tier"] in ("small", "mid")],
+                         ids=lambda k: f"{k['tail']}-{k['top']}")
+def test_memo_kats(kat, corc):
+    """Memo CSR hash vs SURVEY App. A KATs (incl. C3 t=3, 13.5 M rows, whole-grid fill)."""
+    tail, top = parse_gens(kat["tail"]), int(kat["top"])
+    memo = fz.memo_build((7,) + tail, len(tail), top)
+    rows, _, _ = memo.views()
+    assert memo.info["entries"] == int(kat["entries"])
+    assert corc.hash_rows(_np(rows).reshape(-1, len(tail))) == int(kat["H"], 16)
+
+
+# ---------------------------------------------------------------------- C1
+def test_c1_all_m(corc):
+    """C1: Z(m; 6,9,20) for every m <= 1000 from ONE memo (t=2, top 1001), bit-exact."""
+    memo = fz.memo_build(C1_GENS, C1_T, C1_MAX_N + 1)
+    tot, hs = 0, 0
+    for m in range(C1_MAX_N + 1):
+        out, rows, _ = fz.enumerate(memo, m, "materialize")
+        want, cnt, h = corc.enumerate(m, C1_GENS)
+        assert rows == cnt
+        assert np.array_equal(_np(out).reshape(-1, 3)[:rows], want.reshape(-1, 3)), m
+        tot += rows
+        _, _, gh = fz.enumerate(memo, m, "hash")
+        assert gh == h, m
+        hs = (hs + gh) % (1 << 64)
+        assert fz.count(memo, m) == cnt
+    assert tot == 162781 and hs == 0x54C291A6F228CA38      # SURVEY App. A aggregate
+
+
+# -------------------------------------------------------------- random suite
+@pytest.mark.parametrize("seed", range(200))
+def test_random_small(seed, corc):
+    """random (d 2..5, g <= 25, n <= 120) instances, every t in 0..d-1,
+    full memo (top n+1) and a larger top; list, count and hash bit-exact."""
+    g, n, _ = random_instance(seed)
+    want, cnt, h = corc.enumerate(n, g)
+    for t in range(0, len(g)):
+        for top in (n + 1, n + 37):
+            memo = fz.memo_build(g, t, top)
+            out, rows, _ = fz.enumerate(memo, n, "materialize")
+            assert rows == cnt
+            assert np.array_equal(_np(out).reshape(-1, len(g))[:rows], want.reshape(-1, len(g))), (t, top)
+            assert fz.enumerate(memo, n, "hash")[1:] == (cnt, h)
+            assert fz.enumerate(memo, n, "count")[1] == cnt
+            assert fz.count(memo, n) == cnt
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_mid_sharded(seed, corc):
+    """Mid-size Table-1-shaped instances spanning many slices with ragged tails; shard
+    invariance over 1, 2, 3 and 7 shards (concatenation in rank order == the full list)."""
+    g, n, t = random_instance_mid(seed)
+    memo = fz.memo_build(g, t, n + 1)
+    _check_materialize(memo, n, corc, g, shards=(1, 2, 3, 7))
+
+
+# ------------------------------------------------------------------- Table 1
+@pytest.mark.parametrize("d,md,n", TABLE1_ROWS, ids=lambda x: str(x))
+def test_table1_rows(d, md, n, corc):
+    """C5: every Table 1 row with the paper's memo_dim and a full memo
+    (top = n+1): count == oracle (erratum R14 at line 318 -> 779257) and
+    hash == oracle; rows element by element up to 3 M rows."""
+    g = table1_gens(d)
+    memo = fz.memo_build(g, md, n + 1)
+    cnt, h = corc.count_hash(n, g, use_o2=True)
+    out, rows, _ = fz.enumerate(memo, n, "materialize")
+    assert rows == cnt
+    assert fz.enumerate(memo, n, "hash")[1:] == (cnt, h)
+    assert fz.enumerate(memo, n, "count")[1] == cnt
+    got = _np(out).reshape(-1, d)[:rows]
+    if cnt <= 3_000_000:
+        want, _, _ = corc.enumerate(n, g, use_o2=True)
+        assert np.array_equal(got, want)
+    else:
+        assert corc.hash_rows(got) == h      # host recomputation of the hash of the GPU list
+
+
+# ---------------------------------------------------------------------- C2
+def test_c2_full_materialize(corc):
+    """C2 at full size in bench.py's launch configuration: 100 000 681 rows, element by element."""
+    g, n, t = C2.gens, C2.n, C2.t
+    memo = fz.memo_build(g, t, n + 1)
+    out, rows, _ = fz.enumerate(memo, n, "materialize")
+    want, cnt, h = corc.enumerate(n, g, use_o2=True)
+    assert rows == cnt == 100_000_681
+    assert np.array_equal(_np(out).reshape(-1, 4), want)
+    assert h == 0x5FC4E1F53888C565
+    assert fz.enumerate(memo, n, "hash")[1:] == (cnt, h)
+    assert fz.enumerate(memo, n, "count")[1] == cnt
+
+
+# ---------------------------------------------------------------------- C3
+@pytest.mark.parametrize("t", (2, 3))
+def test_c3_count_hash(t, corc):
+    """C3 count+hash: count == GF count, hash == SURVEY App. A KAT, identical for every t."""
+    memo = fz.memo_build(C3_GENS, t, C3_N + 1)
+    _, rows, h = fz.enumerate(memo, C3_N, "hash")
+    assert rows == corc.gf_count(C3_N, C3_GENS) == 10_002_178_949
+    assert h == 0xBE3AEBC0385B7792
+    assert fz.enumerate(memo, C3_N, "count")[1] == rows
+
+
+# ---------------------------------------------------------------------- C4
+def test_c4_count(corc):
+    """C4 count-only, t=3: the walk's count == the independent GF count (3 356 809 984 741)."""
+    memo = fz.memo_build(C4.gens, C4.t, C4.n + 1, entries=False)
+    want = corc.gf_count(C4.n, C4.gens)
+    assert want == 3_356_809_984_741
+    assert fz.enumerate(memo, C4.n, "count")[1] == want
+    assert fz.count(memo, C4.n) == want
+    tot = sum(fz.enumerate(memo, C4.n, "count", shard=s, nshards=8)[1] for s in range(8))
+    assert tot == want
+
+
+def test_c4_shape_hash(corc):
+    """C4-shaped hash pin (n = 10000): 251 416 858 rows, H from SURVEY App. A."""
+    memo = fz.memo_build(C4.gens, 3, 10001)
+    assert fz.enumerate(memo, 10000, "hash")[1:] == (251_416_858, 0x2C3F7155D27A609C)
+
+
+# ----------------------------------------------------------------- edge cases
+EDGE = [((6, 9, 20), 0, 2), ((6, 9, 20), 43, 2), ((6, 9, 20), 44, 1), ((2, 3), 1, 1), ((5,), 35, 0), ((5,), 36, 0),
+        ((1, 1, 1), 50, 1), ((3, 3, 3), 30, 2), ((4, 6), 1000, 1), ((1,), 0, 0), ((7, 7), 700, 0),
+        ((2, 4, 8, 16, 32, 64, 128, 256, 512, 1024), 300, 3)]
+
+
+@pytest.mark.parametrize("g,n,t", EDGE, ids=lambda x: str(x))
+def test_edges(g, n, t, corc):
+    """n = 0, non-representable n, d = 1, g_i = 1, duplicates, gcd > 1, t = 0, d = 10."""
+    memo = fz.memo_build(g, t, n + 1)
+    _check_materialize(memo, n, corc, g, shards=(1, 3))
+
+
+def test_errors():
+    memo = fz.memo_build((6, 9, 20), 2, 101)
+    with pytest.raises(fz.FzError) as e:
+        fz.enumerate(memo, 101, "materialize")          # n >= top
+    assert e.value.status == 1
+    out = torch.empty((3, 3), dtype=torch.int32, device="cuda")
+    with pytest.raises(fz.FzError) as e:
+        fz.enumerate(memo, 100, "materialize", out=out)  # |Z(100)| = 7 > 3 rows
+    assert e.value.status == 4
+    cm = fz.memo_build((6, 9, 20), 2, 101, entries=False)
+    with pytest.raises(fz.FzError):
+        fz.enumerate(cm, 100, "materialize")             # count-only memo
+
+
+def test_run_host_end_to_end(corc):
+    """fz_run_host (host buffers, chunked D2H) == oracle."""
+    for g, n, t in (((13, 37, 38, 40), 5000, 2), ((6, 9, 20), 1000, 2), ((11, 13, 17, 19), 4000, 2)):
+        want, cnt, h = corc.enumerate(n, g)
+        host = torch.empty((cnt, len(g)), dtype=torch.int32).pin_memory()
+        r, hh = fz.run_host(g, t, n, "materialize", host)
+        assert r == cnt
+        assert np.array_equal(host.numpy().view(np.uint32), want)
+        assert fz.run_host(g, t, n, "hash") == (cnt, h)
+        assert fz.run_host(g, t, n, "count")[0] == cnt

@@ -1,0 +1,59 @@
+"""Quick CUDA-event timings of the three phases (memo build, plan, enumerate) on one config.
+Usage: python tools/quick_time.py [C2|C3t2|C3t3|C4|T1]"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2407_20474_b200 import fz  # noqa: E402
+
+CFG = {
+    "C2": ((11, 13, 17, 19), 30232, 2, "materialize"),
+    "C2h": ((11, 13, 17, 19), 30232, 2, "hash"),
+    "C2c": ((11, 13, 17, 19), 30232, 2, "count"),
+    "C3t2": ((23, 29, 31, 37, 41, 43), 17350, 2, "hash"),
+    "C3t3": ((23, 29, 31, 37, 41, 43), 17350, 3, "hash"),
+    "C4": ((97, 98, 99, 100, 101, 102, 103, 104), 40000, 3, "count"),
+    "T1": ((13, 37, 38, 40, 41, 42, 43, 44), 2000, 4, "materialize"),
+}
+
+
+def ev():
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def main():
+    names = sys.argv[1:] or ["C2"]
+    for name in names:
+        g, n, t, mode = CFG[name]
+        for rep in range(4):
+            torch.cuda.synchronize()
+            e0 = ev()
+            memo = fz.memo_build(g, t, n + 1, entries=(mode != "count"))
+            e1 = ev()
+            plan = fz.Plan(memo, n, mode)
+            e2 = ev()
+            out = None
+            if mode == "materialize":
+                out = torch.empty((plan.rows, len(g)), dtype=torch.int32, device="cuda")
+                e2 = ev()
+            plan.launch(out)
+            e3 = ev()
+            torch.cuda.synchronize()
+            rows, h = plan.result()
+            mb, pl, en = e0.elapsed_time(e1), e1.elapsed_time(e2), e2.elapsed_time(e3)
+            extra = ""
+            if mode == "materialize":
+                extra = f" write {rows * len(g) * 4 / en / 1e6:.1f} GB/s"
+            print(f"{name} rep{rep}: memo {mb*1e3:.1f} us (mode {memo.info['fill_mode']}, batches "
+                  f"{memo.info['batches']}, entries {memo.info['entries']}), plan {pl*1e3:.1f} us "
+                  f"({plan.nslices} slices), enum {en*1e3:.1f} us, rows {rows} hash {h:#x} "
+                  f"-> {rows / ((mb + pl + en) / 1e3):.3e} fact/s{extra}", flush=True)
+            del out
+
+
+if __name__ == "__main__":
+    main()
