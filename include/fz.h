@@ -82,6 +82,16 @@ fz_status fz_memo_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t t
 /* Memory cap for memo rows (bytes); 0 restores the default 8e9. */
 void fz_set_memo_cap(uint64_t bytes);
 
+/* A1 as a reusable host object (like an FFT plan): validation, sizing and the
+ * host copy of the count tables for (gens, d, t, top, with_entries).  Building
+ * a memo from a layout (fz_memo_build_layout) launches kernels only, with no
+ * host-side loops.  Same errors as fz_memo_workspace_bytes.  Immutable; must
+ * outlive every memo built from it. */
+typedef struct fz_layout fz_layout;
+fz_status fz_layout_create(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out);
+fz_status fz_layout_workspace_bytes(const fz_layout *lay, uint64_t *bytes);
+void fz_layout_free(fz_layout *lay);
+
 /* ------------------------------------------------------------- A2-A4 -- */
 /* Build the memo on the GPU (asynchronous on `stream`):
  *   K1 count pass: suffix tables S_i[x] = |Z(x; g_i..g_d)| = |Z_{>=i}(x)|
@@ -101,7 +111,11 @@ void fz_set_memo_cap(uint64_t bytes);
 fz_status fz_memo_build(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, void *d_ws,
                         uint64_t ws_bytes, void *stream, fz_memo **out);
 
+/* Same, from a layout (no host work beyond the launches). */
+fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_bytes, void *stream, fz_memo **out);
+
 fz_status fz_memo_get_info(const fz_memo *m, fz_memo_info *info);
+fz_status fz_layout_get_info(const fz_layout *lay, fz_memo_info *info);
 
 /* Device pointers into the memo workspace (read-only views for tests):
  * rows = u32[entries * t] (CSR, x-major, each block descending lex),
@@ -113,21 +127,24 @@ fz_status fz_memo_device_views(const fz_memo *m, const uint32_t **rows, const ui
 fz_status fz_count(const fz_memo *m, uint64_t n, void *stream, uint64_t *count);
 
 /* ---------------------------------------------------------------- A5 -- */
-/* Shard plan of the lexicographic space of Z(n) over `nshards` ranks.
- * MATERIALIZE/HASH split the output rows into nshards contiguous ranges of
- * (almost) equal size; COUNT splits the leading-prefix walk evenly.  Returns,
- * per shard s, the first global row and the row count (host arrays of
- * nshards entries; NULL to skip).  No device work. */
+/* Shard plan of the lexicographic space of Z(n) over `nshards` ranks (host
+ * copy of the same cut K4 makes on the device).  MATERIALIZE/HASH split the
+ * output rows into nshards contiguous ranges, floor(|Z| s / nshards) ..;
+ * COUNT splits the leading-prefix walk evenly.  Returns, per shard s, the
+ * first global row and the row count (host arrays of nshards entries; NULL to
+ * skip).  No device work. */
 fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards, uint64_t *row_begin,
                         uint64_t *rows);
 
-/* Device plan-workspace bytes for (n, mode, nshards). */
-fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t n, fz_mode mode, int nshards, uint64_t *bytes);
+/* Device plan-workspace bytes (a fixed bound: 256-B header + 64 B per slice,
+ * at most 32 x (resident warps) slices). */
+fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t *bytes);
 
-/* K4 planner (asynchronous): cut shard `shard` of `nshards` into bounded
- * slices of equal rows (MATERIALIZE, HASH) or equal leading prefixes (COUNT)
- * and unrank each slice start to its leading prefix (a_1..a_L) and offset in
- * the memo block, from the S / W tables:
+/* K4 planner (asynchronous, entirely on the device): read |Z(n)| (or the
+ * leading-prefix count) from the device tables, cut shard `shard` of
+ * `nshards`, cut it into bounded slices of equal rows (MATERIALIZE, HASH) or
+ * equal leading prefixes (COUNT), and unrank each slice start to its leading
+ * prefix (a_1..a_L) and offset in the memo block, from the S / W tables:
  *   rank(a_1..a_L) = sum_j S_j[ r_{j-1} - (a_j + 1) g_j ],  r_j = n - sum_{i<=j} a_i g_i.
  * Writes the slice table and zeroes the result accumulators in d_plan
  * (>= fz_plan_workspace_bytes, 256-B aligned, caller-owned) and returns a host
@@ -139,8 +156,9 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
                          uint64_t plan_bytes, void *stream, fz_plan **out);
 void fz_plan_free(fz_plan *p);
 
-/* This plan's shard: first global row, row count, number of slices. */
-fz_status fz_plan_get_shard(const fz_plan *p, uint64_t *row_begin, uint64_t *rows, uint64_t *nslices);
+/* This plan's shard as computed on the device: first global row, row count,
+ * number of slices (synchronises `stream`). */
+fz_status fz_plan_shard(const fz_plan *p, void *stream, uint64_t *row_begin, uint64_t *rows, uint64_t *nslices);
 
 /* ------------------------------------------------------------- A6-A9 -- */
 /* K5 enumerator (asynchronous) over a plan: every warp walks its slices'
@@ -149,12 +167,14 @@ fz_status fz_plan_get_shard(const fz_plan *p, uint64_t *row_begin, uint64_t *row
  * looks up Memo[p], p = n - phi(prefix), and
  *   MATERIALIZE: writes prefix ++ Memo[p][k] for each row to
  *                d_out[(row - shard_row_begin) * d ...] (rows of this shard only;
- *                16-B aligned; out_capacity_rows must be >= the shard's rows,
- *                else FZ_ENOSPC);
+ *                aligned to 16 B if 4 | d, 8 B if 2 | d, else 4 B).  If
+ *                out_capacity_rows is below the shard's rows the kernel writes
+ *                nothing and fz_plan_result returns FZ_ENOSPC;
  *   COUNT:       accumulates |Memo[p]| (no memo rows read);
  *   HASH:        accumulates h(row_base + row - shard_row_begin, row) (R17).
- * row_base is the global index the hash uses for this shard's first row
- * (normally the shard's row_begin).  d_out may be NULL unless MATERIALIZE. */
+ * row_base is the global index the hash uses for this shard's first row;
+ * UINT64_MAX (~0) takes the shard's row_begin from the device plan.
+ * d_out may be NULL unless MATERIALIZE. */
 fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_capacity_rows, uint64_t row_base,
                               void *stream);
 

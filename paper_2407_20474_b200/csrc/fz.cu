@@ -17,7 +17,8 @@
 #include "fz_kernels.cuh"
 
 using fzk::Gens;
-using fzk::PlanParams;
+using fzk::PlanArgs;
+using fzk::PlanHdr;
 using fzk::Slice;
 
 namespace {
@@ -107,7 +108,7 @@ fz_status host_tables(const uint32_t *g, int d, int L, uint64_t top, HostTables 
 }
 
 struct Layout {
-    uint64_t S, W, card, off, links, rows, counter, total;
+    uint64_t S, W, cardT, off, offT, chunk, links, rows, counter, total;
 };
 
 struct Sizing {
@@ -115,11 +116,15 @@ struct Sizing {
     uint64_t top;
     uint64_t entries = 0, max_card = 0, window = 0, ring_rows = 0, batches = 0;
     uint32_t batch = 0;
+    uint32_t stage_words = 0;   // fill mode 1: words per TMA link stage
+    uint64_t smem_bytes = 0;    // fill mode 1: dynamic shared memory
     int fill_mode = 0;
     Layout lay{};
 };
 
-constexpr uint64_t kRingBytesMax = 160 * 1024;
+constexpr uint64_t kSmemMax = 220 * 1024;   // dynamic shared memory budget of the ring fill
+constexpr int kRingStages = 8;              // must match k3_fill_ring's NS
+constexpr int kMaxGrid = 1024;              // chunk scratch entries of the K1 grid
 
 fz_status validate(const uint32_t *g, int d, int t, uint64_t top)
 {
@@ -172,26 +177,42 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
             return fail(FZ_ECAP, "memo of %llu rows x %d coords exceeds the cap of %llu bytes",
                         (unsigned long long)entries, t, (unsigned long long)g_memo_cap);
         rows_bytes = entries * 4ull * t;
-        uint64_t ring = 1;
+        uint64_t ring = 4;
         while (ring < win) ring <<= 1;
         z.ring_rows = ring;
+        // mode 1 needs u32 CSR rows, the ring, NS link stages and the batch offsets in shared memory
+        uint64_t sw = 0;
+        for (uint64_t k = 0; k < z.batches; ++k) {
+            uint64_t x0 = k * b, x1 = std::min<uint64_t>(x0 + b, top);
+            uint64_t a0 = off[x0] & ~3ull, a1 = (off[x1] + 3) & ~3ull;
+            sw = std::max(sw, a1 - a0);
+        }
+        z.stage_words = (uint32_t)std::min<uint64_t>(sw, 0xffffffffu);
+        const uint64_t smem = 4 * ((z.batches + 1 + 3) & ~3ull) + ring * 4ull * t + kRingStages * 4ull * sw +
+                              8ull * kRingStages;
+        z.smem_bytes = smem;
         if (entries >= (1ull << 25) || entries / z.batches > 16384)
             z.fill_mode = 3;
-        else if (ring * 4ull * t <= kRingBytesMax)
+        else if (smem <= kSmemMax && entries < (1ull << 31) && ring < (1ull << 27))
             z.fill_mode = 1;
         else
             z.fill_mode = 2;
     } else {
         z.fill_mode = 0;
     }
+    const uint64_t m = g[L - 1];
     Layout &l = z.lay;
     uint64_t p = 256;                                   // header
     l.S = p;       p = align_up(p + 8ull * (d + 1) * top, 256);
     l.W = p;       p = align_up(p + 8ull * (L + 1) * top, 256);
-    l.card = p;    p = align_up(p + 4ull * top, 256);
     l.off = p;     p = align_up(p + 8ull * (top + 1), 256);
+    l.cardT = p;   p = align_up(p + 4ull * (top + m), 256);
+    l.offT = p;    p = align_up(p + 8ull * (top + m), 256);
+    l.chunk = p;   p = align_up(p + 8ull * kMaxGrid, 256);
     l.counter = p; p = align_up(p + 256, 256);
-    l.links = p;   if (z.fill_mode == 1 || z.fill_mode == 2) p = align_up(p + 8ull * entries, 256);
+    l.links = p;
+    if (z.fill_mode == 1) p = align_up(p + 4ull * entries + 64, 256);
+    if (z.fill_mode == 2) p = align_up(p + 8ull * entries, 256);
     l.rows = p;    p = align_up(p + rows_bytes, 256);
     l.total = p;
     return FZ_OK;
@@ -199,24 +220,30 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
 
 }  // namespace
 
-struct fz_memo {
+// A1 result: validated generators + sizing + host tables (kept for host-side
+// shard queries and the end-to-end host API).  Immutable; reusable for many builds.
+struct fz_layout {
     Sizing z;
     uint32_t g[FZ_MAX_D];
     int with_entries;
     HostTables H;
+};
+
+struct fz_memo {
+    const fz_layout *lay;
+    fz_layout *owned;      // layout created by fz_memo_build (freed with the memo)
     char *ws;
-    uint64_t *S, *W, *off;
-    uint32_t *card, *rows;
-    uint64_t *links;
+    uint64_t *S, *W, *off, *offT, *chunk;
+    uint32_t *cardT, *rows;
+    void *links;
     unsigned int *counter;
 };
 
 struct fz_plan {
     const fz_memo *m;
-    PlanParams P;
+    uint64_t n;
     fz_mode mode;
     int shard, nshards;
-    uint64_t shard_row_begin, shard_rows;
     char *d_plan;
 };
 
@@ -230,24 +257,33 @@ Gens make_gens(const uint32_t *g, int d)
     return G;
 }
 
+constexpr uint64_t kPlanHeader = 256;
+
+uint64_t max_slices()
+{
+    return (uint64_t)device_sms() * 8 * (fzk::kWalkThreads / 32) * 4;
+}
+
+uint64_t plan_bytes() { return kPlanHeader + align_up(max_slices() * sizeof(Slice), 256); }
+
+unsigned walk_blocks() { return (unsigned)device_sms() * 8; }
+
 template <int T>
 fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
 {
-    const Sizing &z = m->z;
-    if (z.fill_mode == 1 || z.fill_mode == 2) {
-        const int threads = 1024;
-        const bool ring = z.fill_mode == 1;
-        const size_t smem = ring ? (size_t)(z.ring_rows * 4ull * T) : 0;
-        if (ring) {
-            FZ_CUDA(cudaFuncSetAttribute(fzk::k3_fill_single<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-            fzk::k3_fill_single<T, true><<<1, threads, smem, s>>>(m->off, m->links, m->rows, z.top, z.batch,
-                                                                  z.ring_rows - 1);
-        } else {
-            fzk::k3_fill_single<T, false><<<1, threads, 0, s>>>(m->off, m->links, m->rows, z.top, z.batch, 0);
-        }
+    const Sizing &z = m->lay->z;
+    if (z.fill_mode == 1) {
+        const size_t smem = (size_t)z.smem_bytes;
+        FZ_CUDA(cudaFuncSetAttribute(fzk::k3_fill_ring<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        fzk::k3_fill_ring<T><<<1, 1024, smem, s>>>(m->off, (const uint32_t *)m->links, m->rows, z.top, z.batch,
+                                                   (uint32_t)z.batches, (uint32_t)z.ring_rows, z.stage_words);
         ++g_launches;
-        return cuda_check("k3_fill_single");
+        return cuda_check("k3_fill_ring");
+    }
+    if (z.fill_mode == 2) {
+        fzk::k3_fill_l2<T><<<1, 1024, 0, s>>>(m->off, (const uint64_t *)m->links, m->rows, z.top, z.batch);
+        ++g_launches;
+        return cuda_check("k3_fill_l2");
     }
     if (z.fill_mode == 3) {
         int per_sm = 0;
@@ -255,7 +291,7 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
         if (per_sm < 1) return fail(FZ_ECUDA, "k3_fill_grid cannot be resident");
         int blocks = device_sms() * std::min(per_sm, 4);
         FZ_CUDA(cudaMemsetAsync(m->counter, 0, 256, s));
-        Gens G = make_gens(m->g, z.d);
+        Gens G = make_gens(m->lay->g, z.d);
         int L = z.L;
         uint64_t top = z.top;
         uint32_t b = z.batch;
@@ -273,36 +309,31 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
 template <int T = 1>
 fz_status launch_fill(const fz_memo *m, cudaStream_t s)
 {
+    if (m->lay->z.fill_mode == 0) return FZ_OK;
     if constexpr (T < FZ_MAX_D) {
-        if (m->z.t == T) return launch_fill_t<T>(m, s);
+        if (m->lay->z.t == T) return launch_fill_t<T>(m, s);
         return launch_fill<T + 1>(m, s);
     } else {
-        return fail(FZ_EINVAL, "t=%d not instantiated", m->z.t);
+        return fail(FZ_EINVAL, "t=%d not instantiated", m->lay->z.t);
     }
 }
 
 struct WalkArgs {
     Gens G;
-    PlanParams P;
+    uint64_t n;
+    PlanHdr *hdr;
     const Slice *slices;
-    const uint32_t *card;
-    const uint64_t *off;
-    const uint32_t *memo;
+    fzk::WalkTables wt;
     uint32_t *out;
+    uint64_t cap;
     uint64_t row_base;
-    uint64_t *result;
 };
 
 template <int D, int T, int MODE>
 fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
 {
-    const int threads = fzk::kWalkThreads;
-    uint64_t want = (a.P.nslices * 32 + threads - 1) / threads;
-    int per_sm = 8;
-    uint64_t blocks = std::min<uint64_t>(want, (uint64_t)device_sms() * per_sm);
-    if (blocks == 0) blocks = 1;
-    fzk::k5_walk<D, T, MODE><<<(unsigned)blocks, threads, 0, s>>>(a.G, a.P, a.slices, a.card, a.off, a.memo, a.out,
-                                                                   a.row_base, a.result);
+    fzk::k5_walk<D, T, MODE><<<walk_blocks(), fzk::kWalkThreads, 0, s>>>(a.G, a.n, a.hdr, a.slices, a.wt, a.out,
+                                                                         a.cap, a.row_base);
     ++g_launches;
     return cuda_check("k5_walk");
 }
@@ -335,26 +366,26 @@ fz_status launch_walk(int d, int t, int mode, const WalkArgs &a, cudaStream_t s)
     }
 }
 
-// host-side rank / unrank over the host tables (shard boundaries for COUNT)
-uint64_t host_row_rank(const fz_memo *m, uint64_t n, const uint32_t *a)
+// host-side rank / unrank over the layout's host tables (fz_shard_rows, fz_run_host)
+uint64_t host_row_rank(const fz_layout *lay, uint64_t n, const uint32_t *a)
 {
-    const uint64_t top = m->z.top;
+    const uint64_t top = lay->z.top;
     uint64_t r = n, R = 0;
-    for (int j = 0; j < m->z.L; ++j) {
-        const uint64_t nxt = (uint64_t)(a[j] + 1ull) * m->g[j];
-        if (nxt <= r) R += m->H.S[(size_t)j * top + (r - nxt)];
-        r -= (uint64_t)a[j] * m->g[j];
+    for (int j = 0; j < lay->z.L; ++j) {
+        const uint64_t nxt = (uint64_t)(a[j] + 1ull) * lay->g[j];
+        if (nxt <= r) R += lay->H.S[(size_t)j * top + (r - nxt)];
+        r -= (uint64_t)a[j] * lay->g[j];
     }
     return R;
 }
 
-void host_unrank_prefix(const fz_memo *m, uint64_t n, uint64_t R, uint32_t *a)
+void host_unrank_prefix(const fz_layout *lay, uint64_t n, uint64_t R, uint32_t *a)
 {
-    const uint64_t top = m->z.top;
+    const uint64_t top = lay->z.top;
     uint64_t r = n;
-    for (int j = 0; j < m->z.L; ++j) {
-        const uint64_t *Tj = m->H.W.data() + (size_t)j * top;
-        const uint64_t gj = m->g[j], amax = r / gj;
+    for (int j = 0; j < lay->z.L; ++j) {
+        const uint64_t *Tj = lay->H.W.data() + (size_t)j * top;
+        const uint64_t gj = lay->g[j], amax = r / gj;
         uint64_t lo = 0, hi = amax;   // largest a with Tj[r - a gj] > R
         while (lo < hi) {
             uint64_t mid = lo + (hi - lo + 1) / 2;
@@ -366,51 +397,44 @@ void host_unrank_prefix(const fz_memo *m, uint64_t n, uint64_t R, uint32_t *a)
     }
 }
 
-fz_status shard_units(const fz_memo *m, uint64_t n, fz_mode mode, int nshards, int s, uint64_t &ub, uint64_t &ul,
-                      uint64_t &rb, uint64_t &rl)
+uint64_t mul_div_h(uint64_t U, uint64_t a, uint64_t b) { return (U / b) * a + ((U % b) * a) / b; }
+
+// same shard cut as k4_plan, on the host tables
+void host_shard(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, int s, uint64_t &rb, uint64_t &rl)
 {
-    const uint64_t top = m->z.top;
-    const uint64_t rows_total = m->H.S[n];
+    const uint64_t rows_total = lay->H.S[n];
     if (mode == FZ_COUNT) {
-        const uint64_t P = m->H.W[n];
-        auto cut = [&](int k) { return (uint64_t)((unsigned __int128)P * (unsigned)k / (unsigned)nshards); };
-        ub = cut(s);
-        ul = cut(s + 1) - ub;
+        const uint64_t P = lay->H.W[n];
         auto rowat = [&](uint64_t pidx) -> uint64_t {
             if (pidx >= P) return rows_total;
             uint32_t a[FZ_MAX_D] = {0};
-            host_unrank_prefix(m, n, pidx, a);
-            return host_row_rank(m, n, a);
+            host_unrank_prefix(lay, n, pidx, a);
+            return host_row_rank(lay, n, a);
         };
-        rb = rowat(ub);
-        rl = rowat(ub + ul) - rb;
+        rb = rowat(mul_div_h(P, s, nshards));
+        rl = rowat(mul_div_h(P, s + 1, nshards)) - rb;
     } else {
-        auto cut = [&](int k) { return (uint64_t)((unsigned __int128)rows_total * (unsigned)k / (unsigned)nshards); };
-        ub = cut(s);
-        ul = cut(s + 1) - ub;
-        rb = ub;
-        rl = ul;
+        rb = mul_div_h(rows_total, s, nshards);
+        rl = mul_div_h(rows_total, s + 1, nshards) - rb;
     }
-    (void)top;
+}
+
+fz_status make_layout(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out)
+{
+    *out = nullptr;
+    fz_status st = validate(gens, d, t, top);
+    if (st) return st;
+    fz_layout *lay = new (std::nothrow) fz_layout();
+    if (!lay) return fail(FZ_ECAP, "host allocation failed");
+    for (int i = 0; i < d; ++i) lay->g[i] = gens[i];
+    lay->with_entries = with_entries ? 1 : 0;
+    if ((st = host_tables(gens, d, d - t, top, lay->H)) ||
+        (st = size_memo(gens, d, t, top, with_entries, lay->H, lay->z))) {
+        delete lay;
+        return st;
+    }
+    *out = lay;
     return FZ_OK;
-}
-
-uint64_t slice_len_for(fz_mode mode, uint64_t units)
-{
-    const uint64_t target = (uint64_t)device_sms() * 8 * (fzk::kWalkThreads / 32) * 4;
-    uint64_t len = (units + target - 1) / std::max<uint64_t>(target, 1);
-    const uint64_t floor_len = (mode == FZ_COUNT) ? 1024 : 256;
-    return std::max(len, floor_len);
-}
-
-constexpr uint64_t kPlanHeader = 256;
-
-// plan workspace for a shard of `units` units (shards differ by at most one unit)
-uint64_t plan_bytes_for(fz_mode mode, uint64_t units)
-{
-    const uint64_t len = slice_len_for(mode, units + 1);
-    const uint64_t ns = (units + 1 + len - 1) / len;
-    return kPlanHeader + align_up(ns * sizeof(Slice), 256);
 }
 
 }  // namespace
@@ -422,71 +446,25 @@ const char *fz_last_error(void) { return g_err.c_str(); }
 uint64_t fz_launch_count(void) { return g_launches; }
 void fz_set_memo_cap(uint64_t bytes) { g_memo_cap = bytes ? bytes : 8000000000ull; }
 
-fz_status fz_memo_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t top, int with_entries,
-                                  uint64_t *bytes)
-{
-    if (!bytes) return fail(FZ_EINVAL, "bytes is NULL");
-    fz_status st = validate(gens, d, t, top);
-    if (st) return st;
-    HostTables H;
-    if ((st = host_tables(gens, d, d - t, top, H))) return st;
-    Sizing z;
-    if ((st = size_memo(gens, d, t, top, with_entries, H, z))) return st;
-    *bytes = z.lay.total;
-    return FZ_OK;
-}
-
-fz_status fz_memo_build(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, void *d_ws,
-                        uint64_t ws_bytes, void *stream, fz_memo **out)
+fz_status fz_layout_create(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out)
 {
     if (!out) return fail(FZ_EINVAL, "out is NULL");
-    *out = nullptr;
-    fz_status st = validate(gens, d, t, top);
-    if (st) return st;
-    if (!d_ws || ((uintptr_t)d_ws & 255)) return fail(FZ_EINVAL, "workspace NULL or not 256-byte aligned");
-    fz_memo *m = new (std::nothrow) fz_memo();
-    if (!m) return fail(FZ_ECAP, "host allocation failed");
-    for (int i = 0; i < d; ++i) m->g[i] = gens[i];
-    m->with_entries = with_entries ? 1 : 0;
-    if ((st = host_tables(gens, d, d - t, top, m->H)) || (st = size_memo(gens, d, t, top, with_entries, m->H, m->z))) {
-        delete m;
-        return st;
-    }
-    const Sizing &z = m->z;
-    if (ws_bytes < z.lay.total) {
-        delete m;
-        return fail(FZ_ENOSPC, "workspace %llu B < required %llu B", (unsigned long long)ws_bytes,
-                    (unsigned long long)z.lay.total);
-    }
-    char *w = (char *)d_ws;
-    m->ws = w;
-    m->S = (uint64_t *)(w + z.lay.S);
-    m->W = (uint64_t *)(w + z.lay.W);
-    m->card = (uint32_t *)(w + z.lay.card);
-    m->off = (uint64_t *)(w + z.lay.off);
-    m->counter = (unsigned int *)(w + z.lay.counter);
-    m->links = (uint64_t *)(w + z.lay.links);
-    m->rows = (uint32_t *)(w + z.lay.rows);
-    cudaStream_t s = (cudaStream_t)stream;
-    Gens G = make_gens(m->g, d);
-    fzk::k1_tables<<<1, 1024, 0, s>>>(G, d, z.L, top, m->S, m->W, m->card, m->off);
-    ++g_launches;
-    if ((st = cuda_check("k1_tables"))) { delete m; return st; }
-    if (z.fill_mode == 1 || z.fill_mode == 2) {
-        uint64_t blocks = std::min<uint64_t>((top * 32 + 255) / 256, (uint64_t)device_sms() * 16);
-        fzk::k3_links<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, s>>>(G, z.L, t, top, m->S, m->off, m->links);
-        ++g_launches;
-        if ((st = cuda_check("k3_links"))) { delete m; return st; }
-    }
-    if ((st = launch_fill(m, s))) { delete m; return st; }
-    *out = m;
+    return make_layout(gens, d, t, top, with_entries, out);
+}
+
+void fz_layout_free(fz_layout *lay) { delete lay; }
+
+fz_status fz_layout_workspace_bytes(const fz_layout *lay, uint64_t *bytes)
+{
+    if (!lay || !bytes) return fail(FZ_EINVAL, "NULL argument");
+    *bytes = lay->z.lay.total;
     return FZ_OK;
 }
 
-fz_status fz_memo_get_info(const fz_memo *m, fz_memo_info *info)
+fz_status fz_layout_get_info(const fz_layout *lay, fz_memo_info *info)
 {
-    if (!m || !info) return fail(FZ_EINVAL, "NULL argument");
-    const Sizing &z = m->z;
+    if (!lay || !info) return fail(FZ_EINVAL, "NULL argument");
+    const Sizing &z = lay->z;
     info->d = z.d;
     info->t = z.t;
     info->top = z.top;
@@ -497,6 +475,100 @@ fz_status fz_memo_get_info(const fz_memo *m, fz_memo_info *info)
     info->fill_mode = z.fill_mode;
     info->window_rows = z.window;
     return FZ_OK;
+}
+
+fz_status fz_memo_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t top, int with_entries,
+                                  uint64_t *bytes)
+{
+    if (!bytes) return fail(FZ_EINVAL, "bytes is NULL");
+    fz_layout *lay = nullptr;
+    fz_status st = make_layout(gens, d, t, top, with_entries, &lay);
+    if (st) return st;
+    *bytes = lay->z.lay.total;
+    delete lay;
+    return FZ_OK;
+}
+
+fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_bytes, void *stream, fz_memo **out)
+{
+    if (!out || !lay) return fail(FZ_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (!d_ws || ((uintptr_t)d_ws & 255)) return fail(FZ_EINVAL, "workspace NULL or not 256-byte aligned");
+    const Sizing &z = lay->z;
+    if (ws_bytes < z.lay.total)
+        return fail(FZ_ENOSPC, "workspace %llu B < required %llu B", (unsigned long long)ws_bytes,
+                    (unsigned long long)z.lay.total);
+    fz_memo *m = new (std::nothrow) fz_memo();
+    if (!m) return fail(FZ_ECAP, "host allocation failed");
+    m->lay = lay;
+    char *w = (char *)d_ws;
+    m->ws = w;
+    m->S = (uint64_t *)(w + z.lay.S);
+    m->W = (uint64_t *)(w + z.lay.W);
+    m->off = (uint64_t *)(w + z.lay.off);
+    m->cardT = (uint32_t *)(w + z.lay.cardT);
+    m->offT = (uint64_t *)(w + z.lay.offT);
+    m->chunk = (uint64_t *)(w + z.lay.chunk);
+    m->counter = (unsigned int *)(w + z.lay.counter);
+    m->links = (void *)(w + z.lay.links);
+    m->rows = (uint32_t *)(w + z.lay.rows);
+    cudaStream_t s = (cudaStream_t)stream;
+    Gens G = make_gens(lay->g, z.d);
+    fzk::Tables tb;
+    tb.S = m->S;
+    tb.W = m->W;
+    tb.off = m->off;
+    tb.cardT = m->cardT;
+    tb.offT = m->offT;
+    tb.chunk = m->chunk;
+    tb.links = m->links;
+    tb.top = z.top;
+    tb.m = lay->g[z.L - 1];
+    tb.R = (z.top + tb.m - 1) / tb.m;
+    tb.d = z.d;
+    tb.L = z.L;
+    tb.t = z.t;
+    tb.link_mode = (z.fill_mode == 1) ? 1 : (z.fill_mode == 2 ? 2 : 0);
+    tb.ring_mask = z.ring_rows ? z.ring_rows - 1 : 0;
+    fz_status st = [&]() -> fz_status {
+        FZ_CUDA(cudaMemsetAsync(m->counter, 0, 256, s));
+        unsigned int *counter = m->counter;
+        void *args[] = {&G, &tb, &counter};
+        const int blocks = std::min(device_sms(), kMaxGrid);
+        FZ_CUDA(cudaLaunchCooperativeKernel((const void *)fzk::k1_tables, blocks, 1024, args, 0, s));
+        ++g_launches;
+        return cuda_check("k1_tables");
+    }();
+    if (!st) st = launch_fill(m, s);
+    if (st) {
+        delete m;
+        return st;
+    }
+    *out = m;
+    return FZ_OK;
+}
+
+fz_status fz_memo_build(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, void *d_ws,
+                        uint64_t ws_bytes, void *stream, fz_memo **out)
+{
+    if (!out) return fail(FZ_EINVAL, "out is NULL");
+    *out = nullptr;
+    fz_layout *lay = nullptr;
+    fz_status st = make_layout(gens, d, t, top, with_entries, &lay);
+    if (st) return st;
+    st = fz_memo_build_layout(lay, d_ws, ws_bytes, stream, out);
+    if (st) {
+        delete lay;
+        return st;
+    }
+    (*out)->owned = lay;
+    return FZ_OK;
+}
+
+fz_status fz_memo_get_info(const fz_memo *m, fz_memo_info *info)
+{
+    if (!m) return fail(FZ_EINVAL, "NULL memo");
+    return fz_layout_get_info(m->lay, info);
 }
 
 fz_status fz_memo_device_views(const fz_memo *m, const uint32_t **rows, const uint64_t **off, const uint64_t **S)
@@ -511,7 +583,8 @@ fz_status fz_memo_device_views(const fz_memo *m, const uint32_t **rows, const ui
 fz_status fz_count(const fz_memo *m, uint64_t n, void *stream, uint64_t *count)
 {
     if (!m || !count) return fail(FZ_EINVAL, "NULL argument");
-    if (n >= m->z.top) return fail(FZ_EINVAL, "n=%llu >= top=%llu", (unsigned long long)n, (unsigned long long)m->z.top);
+    if (n >= m->lay->z.top)
+        return fail(FZ_EINVAL, "n=%llu >= top=%llu", (unsigned long long)n, (unsigned long long)m->lay->z.top);
     cudaStream_t s = (cudaStream_t)stream;
     FZ_CUDA(cudaMemcpyAsync(count, m->S + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     FZ_CUDA(cudaStreamSynchronize(s));
@@ -521,88 +594,66 @@ fz_status fz_count(const fz_memo *m, uint64_t n, void *stream, uint64_t *count)
 fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards, uint64_t *row_begin, uint64_t *rows)
 {
     if (!m || nshards < 1) return fail(FZ_EINVAL, "NULL memo or nshards < 1");
-    if (n >= m->z.top) return fail(FZ_EINVAL, "n >= top");
+    if (n >= m->lay->z.top) return fail(FZ_EINVAL, "n >= top");
     for (int s = 0; s < nshards; ++s) {
-        uint64_t ub, ul, rb, rl;
-        shard_units(m, n, mode, nshards, s, ub, ul, rb, rl);
+        uint64_t rb, rl;
+        host_shard(m->lay, n, mode, nshards, s, rb, rl);
         if (row_begin) row_begin[s] = rb;
         if (rows) rows[s] = rl;
     }
     return FZ_OK;
 }
 
-static fz_status plan_params(const fz_memo *m, uint64_t n, fz_mode mode, int shard, int nshards, PlanParams &P,
-                             uint64_t &rb, uint64_t &rl)
-{
-    if (!m) return fail(FZ_EINVAL, "NULL memo");
-    if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode %d", (int)mode);
-    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(FZ_EINVAL, "shard %d of %d", shard, nshards);
-    if (n >= m->z.top) return fail(FZ_EINVAL, "n=%llu >= top=%llu (full memo required)", (unsigned long long)n,
-                                   (unsigned long long)m->z.top);
-    if (mode != FZ_COUNT && m->z.t > 0 && !m->with_entries)
-        return fail(FZ_EINVAL, "memo built without entries; only FZ_COUNT is possible");
-    uint64_t ub, ul;
-    shard_units(m, n, mode, nshards, shard, ub, ul, rb, rl);
-    P.n = n;
-    P.top = m->z.top;
-    P.shard_begin = ub;
-    P.shard_len = ul;
-    P.slice_len = slice_len_for(mode, ul);
-    P.nslices = (ul + P.slice_len - 1) / P.slice_len;
-    P.d = m->z.d;
-    P.t = m->z.t;
-    P.L = m->z.L;
-    P.mode = (int)mode;
-    return FZ_OK;
-}
-
-fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t n, fz_mode mode, int nshards, uint64_t *bytes)
+fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t *bytes)
 {
     if (!bytes) return fail(FZ_EINVAL, "bytes is NULL");
-    uint64_t mx = 0;
-    for (int s = 0; s < std::max(nshards, 1); ++s) {
-        PlanParams P;
-        uint64_t rb, rl;
-        fz_status st = plan_params(m, n, mode, s, nshards, P, rb, rl);
-        if (st) return st;
-        mx = std::max(mx, P.nslices);
-    }
-    *bytes = kPlanHeader + align_up(mx * sizeof(Slice), 256);
+    (void)m;
+    *bytes = plan_bytes();
     return FZ_OK;
 }
 
 fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, int nshards, void *d_plan,
-                         uint64_t plan_bytes, void *stream, fz_plan **out)
+                         uint64_t plan_ws_bytes, void *stream, fz_plan **out)
 {
     if (!out) return fail(FZ_EINVAL, "out is NULL");
     *out = nullptr;
+    if (!m) return fail(FZ_EINVAL, "NULL memo");
+    if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode %d", (int)mode);
+    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(FZ_EINVAL, "shard %d of %d", shard, nshards);
+    const Sizing &z = m->lay->z;
+    if (n >= z.top)
+        return fail(FZ_EINVAL, "n=%llu >= top=%llu (full memo required)", (unsigned long long)n,
+                    (unsigned long long)z.top);
+    if (mode != FZ_COUNT && z.t > 0 && z.fill_mode == 0)
+        return fail(FZ_EINVAL, "memo built without entries; only FZ_COUNT is possible");
     if (!d_plan || ((uintptr_t)d_plan & 255)) return fail(FZ_EINVAL, "plan workspace NULL or misaligned");
-    PlanParams P;
-    uint64_t rb, rl;
-    fz_status st = plan_params(m, n, mode, shard, nshards, P, rb, rl);
-    if (st) return st;
-    const uint64_t need = kPlanHeader + align_up(P.nslices * sizeof(Slice), 256);
-    if (plan_bytes < need)
-        return fail(FZ_ENOSPC, "plan workspace %llu B < required %llu B", (unsigned long long)plan_bytes,
-                    (unsigned long long)need);
+    if (plan_ws_bytes < plan_bytes())
+        return fail(FZ_ENOSPC, "plan workspace %llu B < required %llu B", (unsigned long long)plan_ws_bytes,
+                    (unsigned long long)plan_bytes());
     fz_plan *p = new (std::nothrow) fz_plan();
     if (!p) return fail(FZ_ECAP, "host allocation failed");
     p->m = m;
-    p->P = P;
+    p->n = n;
     p->mode = mode;
     p->shard = shard;
     p->nshards = nshards;
-    p->shard_row_begin = rb;
-    p->shard_rows = rl;
     p->d_plan = (char *)d_plan;
-    cudaStream_t s = (cudaStream_t)stream;
-    uint64_t *result = (uint64_t *)p->d_plan;
-    Slice *slices = (Slice *)(p->d_plan + kPlanHeader);
-    Gens G = make_gens(m->g, m->z.d);
-    uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((P.nslices * 32 + 255) / 256, 4096));
-    fzk::k4_plan<<<(unsigned)blocks, 256, 0, s>>>(G, P, m->S, m->W, slices, result);
+    PlanArgs A;
+    A.n = n;
+    A.top = z.top;
+    A.max_slices = max_slices();
+    A.floor_len = (mode == FZ_COUNT) ? 1024 : 256;
+    A.mode = (int)mode;
+    A.shard = shard;
+    A.nshards = nshards;
+    A.L = z.L;
+    Gens G = make_gens(m->lay->g, z.d);
+    const unsigned blocks = (unsigned)std::min<uint64_t>((A.max_slices * 32 + 255) / 256, 4096);
+    fzk::k4_plan<<<blocks, 256, 0, (cudaStream_t)stream>>>(G, A, m->S, m->W, (PlanHdr *)p->d_plan,
+                                                           (Slice *)(p->d_plan + kPlanHeader));
     ++g_launches;
-    if ((st = cuda_check("k4_plan"))) {
+    fz_status st = cuda_check("k4_plan");
+    if (st) {
         delete p;
         return st;
     }
@@ -612,12 +663,16 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
 
 void fz_plan_free(fz_plan *p) { delete p; }
 
-fz_status fz_plan_get_shard(const fz_plan *p, uint64_t *row_begin, uint64_t *rows, uint64_t *nslices)
+fz_status fz_plan_shard(const fz_plan *p, void *stream, uint64_t *row_begin, uint64_t *rows, uint64_t *nslices)
 {
     if (!p) return fail(FZ_EINVAL, "NULL plan");
-    if (row_begin) *row_begin = p->shard_row_begin;
-    if (rows) *rows = p->shard_rows;
-    if (nslices) *nslices = p->P.nslices;
+    PlanHdr h;
+    cudaStream_t s = (cudaStream_t)stream;
+    FZ_CUDA(cudaMemcpyAsync(&h, p->d_plan, sizeof h, cudaMemcpyDeviceToHost, s));
+    FZ_CUDA(cudaStreamSynchronize(s));
+    if (row_begin) *row_begin = h.row_begin;
+    if (rows) *rows = h.rows;
+    if (nslices) *nslices = h.nslices;
     return FZ_OK;
 }
 
@@ -626,36 +681,39 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
 {
     if (!p) return fail(FZ_EINVAL, "NULL plan");
     const fz_memo *m = p->m;
+    const Sizing &z = m->lay->z;
     if (p->mode == FZ_MATERIALIZE) {
-        if (!d_out && p->shard_rows) return fail(FZ_EINVAL, "d_out is NULL");
-        if (((uintptr_t)d_out & 15)) return fail(FZ_EINVAL, "d_out not 16-byte aligned");
-        if (out_capacity_rows < p->shard_rows)
-            return fail(FZ_ENOSPC, "output holds %llu rows, shard has %llu", (unsigned long long)out_capacity_rows,
-                        (unsigned long long)p->shard_rows);
+        const uintptr_t align = (z.d % 4 == 0) ? 16 : (z.d % 2 == 0 ? 8 : 4);
+        if (!d_out && out_capacity_rows) return fail(FZ_EINVAL, "d_out is NULL");
+        if (((uintptr_t)d_out & (align - 1))) return fail(FZ_EINVAL, "d_out not %d-byte aligned", (int)align);
     }
-    if (p->P.nslices == 0) return FZ_OK;
     WalkArgs a;
-    a.G = make_gens(m->g, m->z.d);
-    a.P = p->P;
+    a.G = make_gens(m->lay->g, z.d);
+    a.n = p->n;
+    a.hdr = (PlanHdr *)p->d_plan;
     a.slices = (const Slice *)(p->d_plan + kPlanHeader);
-    a.card = m->card;
-    a.off = m->off;
-    a.memo = m->rows;
+    a.wt.cardT = m->cardT;
+    a.wt.offT = m->offT;
+    a.wt.memo = m->rows;
+    a.wt.R = (z.top + m->lay->g[z.L - 1] - 1) / m->lay->g[z.L - 1];
     a.out = d_out;
+    a.cap = (p->mode == FZ_MATERIALIZE) ? out_capacity_rows : ~0ull;
     a.row_base = row_base;
-    a.result = (uint64_t *)p->d_plan;
-    return launch_walk(m->z.d, m->z.t, (int)p->mode, a, (cudaStream_t)stream);
+    return launch_walk(z.d, z.t, (int)p->mode, a, (cudaStream_t)stream);
 }
 
 fz_status fz_plan_result(const fz_plan *p, void *stream, uint64_t *rows, uint64_t *hash)
 {
     if (!p) return fail(FZ_EINVAL, "NULL plan");
-    uint64_t h[2] = {0, 0};
+    PlanHdr h;
     cudaStream_t s = (cudaStream_t)stream;
-    FZ_CUDA(cudaMemcpyAsync(h, p->d_plan, sizeof h, cudaMemcpyDeviceToHost, s));
+    FZ_CUDA(cudaMemcpyAsync(&h, p->d_plan, sizeof h, cudaMemcpyDeviceToHost, s));
     FZ_CUDA(cudaStreamSynchronize(s));
-    if (rows) *rows = h[0];
-    if (hash) *hash = h[1];
+    if (h.err)
+        return fail(FZ_ENOSPC, "output buffer smaller than the shard's %llu rows (nothing written)",
+                    (unsigned long long)h.rows);
+    if (rows) *rows = h.result[0];
+    if (hash) *hash = h.result[1];
     return FZ_OK;
 }
 
@@ -667,11 +725,11 @@ fz_status fz_plan_result_ptr(const fz_plan *p, uint64_t **d_result)
 }
 
 fz_status fz_enumerate(const fz_memo *m, uint64_t n, fz_mode mode, int shard, int nshards, uint64_t row_base,
-                       uint32_t *d_out, uint64_t out_capacity_rows, void *d_plan, uint64_t plan_bytes, void *stream,
+                       uint32_t *d_out, uint64_t out_capacity_rows, void *d_plan, uint64_t plan_ws_bytes, void *stream,
                        uint64_t *rows_out, uint64_t *hash_out)
 {
     fz_plan *p = nullptr;
-    fz_status st = fz_plan_create(m, n, mode, shard, nshards, d_plan, plan_bytes, stream, &p);
+    fz_status st = fz_plan_create(m, n, mode, shard, nshards, d_plan, plan_ws_bytes, stream, &p);
     if (st) return st;
     st = fz_enumerate_launch(p, d_out, out_capacity_rows, row_base, stream);
     if (!st) st = fz_plan_result(p, stream, rows_out, hash_out);
@@ -685,18 +743,14 @@ static constexpr int kRunChunks = 8;
 fz_status fz_run_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, uint64_t *bytes)
 {
     if (!bytes) return fail(FZ_EINVAL, "bytes is NULL");
-    uint64_t memo_b = 0;
-    fz_status st = fz_memo_workspace_bytes(gens, d, t, n + 1, mode != FZ_COUNT, &memo_b);
+    fz_layout *lay = nullptr;
+    fz_status st = make_layout(gens, d, t, n + 1, mode != FZ_COUNT, &lay);
     if (st) return st;
-    HostTables H;
-    if ((st = host_tables(gens, d, d - t, n + 1, H))) return st;
-    const uint64_t rows = H.S[n];
+    const uint64_t rows = lay->H.S[n];
     const int chunks = (mode == FZ_MATERIALIZE) ? kRunChunks : 1;
-    const uint64_t units = (mode == FZ_COUNT) ? H.W[n] : rows;
-    const uint64_t plan_b = align_up(plan_bytes_for(mode, (units + chunks - 1) / chunks), 256);
-    uint64_t out_b = 0;
-    if (mode == FZ_MATERIALIZE) out_b = align_up(rows * 4ull * d, 256);
-    *bytes = align_up(memo_b, 256) + plan_b * chunks + out_b;
+    uint64_t out_b = (mode == FZ_MATERIALIZE) ? align_up(rows * 4ull * d, 256) : 0;
+    *bytes = align_up(lay->z.lay.total, 256) + plan_bytes() * chunks + out_b;
+    delete lay;
     return FZ_OK;
 }
 
@@ -704,29 +758,34 @@ fz_status fz_run_host(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mo
                       uint32_t *h_out, uint64_t h_out_capacity_rows, void *stream, uint64_t *rows_out,
                       uint64_t *hash_out)
 {
-    uint64_t need = 0;
-    fz_status st = fz_run_workspace_bytes(gens, d, t, n, mode, &need);
+    if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode");
+    fz_layout *lay = nullptr;
+    fz_status st = make_layout(gens, d, t, n + 1, mode != FZ_COUNT, &lay);
     if (st) return st;
-    if (ws_bytes < need) return fail(FZ_ENOSPC, "workspace %llu B < %llu B", (unsigned long long)ws_bytes,
-                                     (unsigned long long)need);
-    uint64_t memo_b = 0;
-    if ((st = fz_memo_workspace_bytes(gens, d, t, n + 1, mode != FZ_COUNT, &memo_b))) return st;
-    char *w = (char *)d_ws;
-    cudaStream_t s = (cudaStream_t)stream;
-    fz_memo *m = nullptr;
-    if ((st = fz_memo_build(gens, d, t, n + 1, mode != FZ_COUNT, w, memo_b, stream, &m))) return st;
-    const uint64_t rows_total = m->H.S[n];
+    const uint64_t rows_total = lay->H.S[n];
+    const int chunks = (mode == FZ_MATERIALIZE) ? kRunChunks : 1;
+    const uint64_t memo_b = align_up(lay->z.lay.total, 256);
+    const uint64_t need = memo_b + plan_bytes() * chunks +
+                          ((mode == FZ_MATERIALIZE) ? align_up(rows_total * 4ull * d, 256) : 0);
+    if (ws_bytes < need) {
+        delete lay;
+        return fail(FZ_ENOSPC, "workspace %llu B < %llu B", (unsigned long long)ws_bytes, (unsigned long long)need);
+    }
     if (mode == FZ_MATERIALIZE && (!h_out || h_out_capacity_rows < rows_total)) {
-        fz_free(m);
+        delete lay;
         return fail(FZ_ENOSPC, "host output holds %llu rows, |Z(n)| = %llu", (unsigned long long)h_out_capacity_rows,
                     (unsigned long long)rows_total);
     }
-    char *plan_area = w + align_up(memo_b, 256);
-    const int chunks = (mode == FZ_MATERIALIZE) ? kRunChunks : 1;
-    uint64_t plan_b = 0;
-    if ((st = fz_plan_workspace_bytes(m, n, mode, chunks, &plan_b))) { fz_free(m); return st; }
-    plan_b = align_up(plan_b, 256);
-    uint32_t *d_out = (uint32_t *)(plan_area + plan_b * chunks);
+    char *w = (char *)d_ws;
+    cudaStream_t s = (cudaStream_t)stream;
+    fz_memo *m = nullptr;
+    if ((st = fz_memo_build_layout(lay, w, memo_b, stream, &m))) {
+        delete lay;
+        return st;
+    }
+    m->owned = lay;
+    char *plan_area = w + memo_b;
+    uint32_t *d_out = (uint32_t *)(plan_area + plan_bytes() * chunks);
     cudaStream_t cs = nullptr;
     std::vector<cudaEvent_t> ev(chunks, nullptr);
     if (mode == FZ_MATERIALIZE) {
@@ -736,15 +795,16 @@ fz_status fz_run_host(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mo
     uint64_t tot_rows = 0, tot_hash = 0;
     std::vector<fz_plan *> plans(chunks, nullptr);
     for (int c = 0; c < chunks && !st; ++c) {
-        st = fz_plan_create(m, n, mode, c, chunks, plan_area + plan_b * c, plan_b, stream, &plans[c]);
+        st = fz_plan_create(m, n, mode, c, chunks, plan_area + plan_bytes() * c, plan_bytes(), stream, &plans[c]);
         if (st) break;
-        const uint64_t rb = plans[c]->shard_row_begin;
-        st = fz_enumerate_launch(plans[c], d_out + rb * (uint64_t)d, rows_total - rb, rb, stream);
+        uint64_t rb = 0, rl = 0;
+        host_shard(lay, n, mode, chunks, c, rb, rl);
+        st = fz_enumerate_launch(plans[c], d_out + rb * (uint64_t)d, rows_total - rb, ~0ull, stream);
         if (st) break;
-        if (mode == FZ_MATERIALIZE && plans[c]->shard_rows) {
+        if (mode == FZ_MATERIALIZE && rl) {
             if (cudaEventRecord(ev[c], s) != cudaSuccess || cudaStreamWaitEvent(cs, ev[c], 0) != cudaSuccess ||
-                cudaMemcpyAsync(h_out + rb * (uint64_t)d, d_out + rb * (uint64_t)d,
-                                plans[c]->shard_rows * 4ull * d, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+                cudaMemcpyAsync(h_out + rb * (uint64_t)d, d_out + rb * (uint64_t)d, rl * 4ull * d,
+                                cudaMemcpyDeviceToHost, cs) != cudaSuccess)
                 st = cuda_check("chunk D2H");
         }
     }
@@ -769,6 +829,11 @@ fz_status fz_run_host(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mo
     return FZ_OK;
 }
 
-void fz_free(fz_memo *m) { delete m; }
+void fz_free(fz_memo *m)
+{
+    if (!m) return;
+    delete m->owned;
+    delete m;
+}
 
 }  // extern "C"

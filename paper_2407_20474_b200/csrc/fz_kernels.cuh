@@ -2,23 +2,25 @@
 //
 // Everything here is integer work (no tensor cores: nothing is a dense
 // contraction).  Kernel map:
-//   K1  k1_tables       count pass: suffix tables S_i, prefix tables W_i, card,
-//                       CSR offsets (K2) -- one CTA, column scans over the
-//                       residue classes of g_i.
-//   K3a k3_links        per memo row: the source row of the copy-increment and
-//                       the incremented index (fully parallel; depends only on
-//                       the count tables).
-//   K3b k3_fill_single  the dimensionwise recurrence Z(x) = U_i incr_i(Z_{>=i}(x-g_i))
-//       k3_fill_grid    (Alg. 2/3 PAPER.md:139-192) in elementwise
-//                       batches of b = min(tail g); one CTA with
-//                       the live window in a shared-memory ring, or the whole grid
-//                       with a grid barrier between batches for huge memos.
+//   K1  k1_tables       count pass + CSR + links, one cooperative grid: suffix
+//                       tables S_i and prefix tables W_i by column scans over the
+//                       residue classes of g_i, card
+//                       and CSR offsets (K2) -- also in a residue-major copy for
+//                       the walk -- and, per memo row, the copy-increment source
+//                       ("link") of the recurrence.
+//   K3  k3_fill_ring    the dimensionwise recurrence Z(x) = U_i incr_i(Z_{>=i}(x-g_i))
+//       k3_fill_l2      (Alg. 2/3) in elementwise
+//       k3_fill_grid    batches of b = min(tail g): one CTA with
+//                       the live window in a shared-memory ring and TMA-prefetched
+//                       links; one CTA through L2; or the whole grid with a grid
+//                       barrier between batches for huge memos.
 //   K4  k4_plan         slice planner: unrank each slice start (rows or leading
 //                       prefixes) to its leading prefix + memo offset.
 //   K5  k5_walk         enumerator: nextCandidate over the leading coordinates
 //                       (PAPER.md:203-222, 238-265), innermost leading coordinate
-//                       across the 32 lanes, memo blocks flattened across the warp
-//                       so that every store instruction writes 32 consecutive rows.
+//                       across the 32 lanes (contiguous in the residue-major
+//                       tables), memo blocks flattened across the warp so that every
+//                       store instruction writes 32 consecutive rows.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -30,6 +32,8 @@ namespace fzk {
 constexpr int kMaxD = FZ_MAX_D;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint64_t kLinkMask = (1ull << 56) - 1;
+constexpr uint32_t kRingIdxBits = 27;
+constexpr uint32_t kZeroLink32 = 0xffffffffu;
 
 struct Gens {
     uint32_t g[kMaxD];
@@ -44,14 +48,43 @@ struct Slice {
 };
 static_assert(sizeof(Slice) == 64, "slice layout");
 
-struct PlanParams {
+// Plan header (first 256 B of a plan workspace): written by K4, read by K5.
+struct PlanHdr {
+    uint64_t result[2];    // {rows, hash}: K5 accumulators
+    uint64_t err;          // nonzero: the output buffer is too small (nothing written)
+    uint64_t total_units;  // rows (MAT/HASH) or leading prefixes (COUNT) of all of Z(n)
+    uint64_t shard_begin;  // first unit of this shard
+    uint64_t shard_len;    // units in this shard
+    uint64_t slice_len;    // units per slice
+    uint64_t nslices;
+    uint64_t row_begin;    // global row index of the shard's first row
+    uint64_t rows;         // rows of Z(n) in this shard
+};
+static_assert(sizeof(PlanHdr) <= 256, "plan header");
+
+struct PlanArgs {
     uint64_t n;
     uint64_t top;
-    uint64_t shard_begin;   // global index (row or prefix) of this shard's first unit
-    uint64_t shard_len;     // units in this shard
-    uint64_t slice_len;     // units per slice
-    uint64_t nslices;
-    int d, t, L, mode;
+    uint64_t max_slices;
+    uint64_t floor_len;
+    int mode, shard, nshards, L;
+};
+
+// Pointers and sizes of the count tables (all in the memo workspace).
+struct Tables {
+    uint64_t *S;        // (d+1) x top, natural layout
+    uint64_t *W;        // (L+1) x top
+    uint64_t *off;      // top+1, natural layout (CSR of the memo)
+    uint32_t *cardT;    // top, residue-major w.r.t. m = g_L (innermost leading generator)
+    uint64_t *offT;     // top, residue-major
+    uint64_t *chunk;    // gridDim scratch for the offset scan
+    void *links;        // entries (u32 ring links or u64 row links), or nullptr
+    uint64_t top;
+    uint32_t m;         // g_L
+    uint64_t R;         // rows per residue column = ceil(top / m)
+    int d, L, t;
+    int link_mode;      // 0 none, 1 u32 ring-relative, 2 u64 absolute
+    uint64_t ring_mask;
 };
 
 // ------------------------------------------------------------------ helpers
@@ -59,6 +92,13 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src)
 {
     uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src);
     uint32_t hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int o)
+{
+    uint32_t lo = __shfl_up_sync(kFull, (uint32_t)v, o);
+    uint32_t hi = __shfl_up_sync(kFull, (uint32_t)(v >> 32), o);
     return ((uint64_t)hi << 32) | lo;
 }
 
@@ -73,122 +113,181 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v)
     return v;
 }
 
-__device__ __forceinline__ uint64_t ld_cg_u64(const uint64_t *p) { return __ldcg(p); }
-
-// Column-wise inclusive scan used by the count pass:
-//   dst[x] = src[x] + dst[x - g]   (x >= g),   dst[x] = src[x]   (x < g),  x in [0, N).
-// Viewing [0, N) as a row-major matrix with g columns, this is an inclusive
-// scan down every column (= every residue class mod g).  Three phases: per
-// (column, row segment) partial sums; a warp-level scan of the segment sums of
-// each column; re-scan of each segment with its offset.  One CTA.
-__device__ void column_scan(const uint64_t *src, uint64_t *dst, uint64_t N, uint64_t g, uint64_t *sm)
+// Block-wide exclusive scan of one u64 per thread (blockDim multiple of 32).
+// Returns the exclusive prefix; *total gets the block sum.  Uses sm[33].
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t *sm, uint64_t *total)
 {
-    const int nt = blockDim.x, tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
-    const uint64_t cols_total = g < N ? g : N;
-    const uint64_t rows = (N + g - 1) / g;
-    for (uint64_t c0 = 0; c0 < cols_total; c0 += (uint64_t)nt) {
-        const int ncols = (int)((cols_total - c0) < (uint64_t)nt ? (cols_total - c0) : (uint64_t)nt);
-        const int nseg = nt / ncols;
-        const uint64_t R = (rows + nseg - 1) / nseg;
-        const int ci = tid % ncols, seg = tid / ncols;
-        const bool active = seg < nseg;
-        const uint64_t col = c0 + ci;
-        uint64_t s = 0;
-        if (active) {
-            uint64_t k0 = (uint64_t)seg * R, k1 = k0 + R < rows ? k0 + R : rows;
-#pragma unroll 8
-            for (uint64_t k = k0; k < k1; ++k) {
-                uint64_t x = k * g + col;
-                if (x < N) s += ld_cg_u64(src + x);
-            }
-        }
-        sm[tid] = s;
-        __syncthreads();
-        // phase 2: exclusive scan of the nseg segment sums of each column (warp per column)
-        for (int c = warp; c < ncols; c += nwarps) {
-            uint64_t carry = 0;
-            for (int s0 = 0; s0 < nseg; s0 += 32) {
-                int sg = s0 + lane;
-                uint64_t v = sg < nseg ? sm[sg * ncols + c] : 0;
-                uint64_t inc = v;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    uint64_t inc = v;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    uint64_t u = shfl_u64(inc, (lane - o) & 31);
-                    if (lane >= o) inc += u;
-                }
-                if (sg < nseg) sm[sg * ncols + c] = carry + inc - v;
-                carry += shfl_u64(inc, 31);
-            }
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t u = shfl_up_u64(inc, o);
+        if (lane >= o) inc += u;
+    }
+    if (lane == 31) sm[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t w = lane < nwarps ? sm[lane] : 0;
+        uint64_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t u = shfl_up_u64(wi, o);
+            if (lane >= o) wi += u;
         }
-        __syncthreads();
-        if (active) {
-            uint64_t run = sm[tid];
-            uint64_t k0 = (uint64_t)seg * R, k1 = k0 + R < rows ? k0 + R : rows;
-#pragma unroll 8
-            for (uint64_t k = k0; k < k1; ++k) {
-                uint64_t x = k * g + col;
-                if (x < N) {
-                    run += ld_cg_u64(src + x);
-                    dst[x] = run;
-                }
-            }
+        if (lane < nwarps) sm[lane] = wi - w;
+        if (lane == 31) sm[32] = wi;
+    }
+    __syncthreads();
+    const uint64_t res = sm[warp] + inc - v;
+    *total = sm[32];
+    __syncthreads();
+    return res;
+}
+
+// Grid barrier for a cooperative launch (all CTAs co-resident).  `counter`
+// grows monotonically; `target` is the per-CTA running target.
+__device__ __forceinline__ void grid_barrier(unsigned int *counter, unsigned int &target)
+{
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1u);
+        unsigned int v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+            if ((int)(v - target) >= 0) break;
+            __nanosleep(32);
         }
-        __syncthreads();
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Inclusive scan down one residue column c of a level:
+//   dst[x] = src[x] + dst[x - g]  for x = c, c+g, c+2g, ... < N.   One CTA.
+__device__ void block_column_scan(const uint64_t *src, uint64_t *dst, uint64_t N, uint64_t g, uint64_t c, uint64_t *sm)
+{
+    constexpr int E = 8;
+    const uint64_t rows = (N - c + g - 1) / g;
+    const uint64_t nt = blockDim.x;
+    uint64_t carry = 0;
+    for (uint64_t k0 = 0; k0 < rows; k0 += nt * E) {
+        const uint64_t kb = k0 + threadIdx.x * (uint64_t)E;
+        uint64_t v[E];
+        uint64_t s = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint64_t k = kb + e;
+            v[e] = k < rows ? __ldcg(src + c + k * g) : 0;
+            s += v[e];
+        }
+        uint64_t tot;
+        uint64_t run = carry + block_excl_scan(s, sm, &tot);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint64_t k = kb + e;
+            run += v[e];
+            if (k < rows) dst[c + k * g] = run;
+        }
+        carry += tot;
     }
 }
 
 // ------------------------------------------------------------------ K1 + K2
-// S level i (0-based, i = 0..d) at S + i*top: S_i[x] = |Z(x; g_i..g_{d-1})|, S_d[x] = [x = 0].
-// W level j (j = 0..L) at W + j*top: W_j[x] = #{(a_j..a_{L-1}) : sum a g <= x}, W_L[x] = 1.
-// card[x] = S_L[x] (u32), off[x] = sum_{y<x} card[y], off[top] = entries.
-__global__ void __launch_bounds__(1024) k1_tables(Gens G, int d, int L, uint64_t top, uint64_t *S, uint64_t *W,
-                                                   uint32_t *card, uint64_t *off)
+// One cooperative launch (all CTAs co-resident), phases separated by grid barriers:
+//   S_d[x] = [x = 0], W_L[x] = 1;
+//   phase p = 0..d-1: S_{d-1-p} = column scan of S_{d-p} mod g_{d-1-p}, and W_{L-1-p} likewise;
+//   card = S_L, off = exclusive scan of card (two phases), residue-major cardT/offT;
+//   links: per memo row, the source row of the copy-increment (see k3_fill_*).
+__global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned int *counter)
 {
-    __shared__ uint64_t sm[1024];
-    const int nt = blockDim.x, tid = threadIdx.x;
-    for (uint64_t x = tid; x < top; x += nt) {
-        S[(uint64_t)d * top + x] = (x == 0) ? 1ull : 0ull;
-        if (W) W[(uint64_t)L * top + x] = 1ull;
+    __shared__ uint64_t sm[40];
+    unsigned int target = 0;
+    const uint64_t top = tb.top;
+    const int d = tb.d, L = tb.L;
+    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t x = gt; x < top; x += ng) {
+        tb.S[(uint64_t)d * top + x] = (x == 0) ? 1ull : 0ull;
+        tb.W[(uint64_t)L * top + x] = 1ull;
     }
-    __syncthreads();
-    for (int i = d - 1; i >= 0; --i) column_scan(S + (uint64_t)(i + 1) * top, S + (uint64_t)i * top, top, G.g[i], sm);
-    if (W)
-        for (int j = L - 1; j >= 0; --j)
-            column_scan(W + (uint64_t)(j + 1) * top, W + (uint64_t)j * top, top, G.g[j], sm);
-    const uint64_t *cardS = S + (uint64_t)L * top;
-    for (uint64_t x = tid; x < top; x += nt) card[x] = (uint32_t)ld_cg_u64(cardS + x);
-    // K2: CSR offsets = exclusive scan of card; inclusive scan into off[1..top]
-    column_scan(cardS, off + 1, top, 1, sm);
-    if (tid == 0) off[0] = 0;
-}
-
-// ---------------------------------------------------------------------- K3a
-// links[off[x] + q] = (src row) | (i << 56) for every row q of Z(x; tail), x in [1, top).
-// Block i (0-based tail index) of Z(x) starts at card[x] - S_{L+i}[x]; its k-th
-// row is incr_i of row off[y] + card[y] - S_{L+i}[y] + k = off[y+1] - S_{L+i}[y] + k
-// of Z(y), y = x - g_{L+i}  ("beginning index of Z_{>=i}").
-__global__ void __launch_bounds__(256) k3_links(Gens G, int L, int t, uint64_t top, const uint64_t *__restrict__ S,
-                                                 const uint64_t *__restrict__ off, uint64_t *__restrict__ links)
-{
-    const int lane = threadIdx.x & 31;
-    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    if (gw == 0 && lane == 0) links[0] = ~0ull;   // Memo[0] = [0]: the base case row
+    grid_barrier(counter, target);
+    for (int p = 0; p < d; ++p) {
+        const int i = d - 1 - p, j = L - 1 - p;
+        const uint64_t gi = G.g[i];
+        const uint64_t ncolS = gi < top ? gi : top;
+        const uint64_t gj = j >= 0 ? G.g[j] : 1;
+        const uint64_t ncolW = j >= 0 ? (gj < top ? gj : top) : 0;
+        for (uint64_t c = blockIdx.x; c < ncolS + ncolW; c += gridDim.x) {
+            if (c < ncolS)
+                block_column_scan(tb.S + (uint64_t)(i + 1) * top, tb.S + (uint64_t)i * top, top, gi, c, sm);
+            else
+                block_column_scan(tb.W + (uint64_t)(j + 1) * top, tb.W + (uint64_t)j * top, top, gj, c - ncolS, sm);
+        }
+        grid_barrier(counter, target);
+    }
+    // K2: off = exclusive scan of card = S_L over [0, top); chunk per CTA.
+    const uint64_t *card = tb.S + (uint64_t)L * top;
+    const uint64_t CH = (top + gridDim.x - 1) / gridDim.x;
+    const uint64_t c0 = blockIdx.x * CH, c1 = (c0 + CH < top) ? c0 + CH : top;
+    {
+        uint64_t s = 0;
+        for (uint64_t x = c0 + threadIdx.x; x < c1; x += blockDim.x) s += __ldcg(card + x);
+        uint64_t tot;
+        block_excl_scan(s, sm, &tot);
+        if (threadIdx.x == 0) tb.chunk[blockIdx.x] = tot;
+    }
+    grid_barrier(counter, target);
+    {
+        uint64_t pre = 0;
+        for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += __ldcg(tb.chunk + b);
+        uint64_t tot;
+        pre = block_excl_scan(pre, sm, &tot);   // reduce: tot = sum of chunk[0..bid)
+        pre = tot;
+        const uint64_t m = tb.m;
+        for (uint64_t xb = c0; xb < c1; xb += blockDim.x) {
+            const uint64_t x = xb + threadIdx.x;
+            const uint64_t v = x < c1 ? __ldcg(card + x) : 0;
+            uint64_t t2;
+            const uint64_t ex = pre + block_excl_scan(v, sm, &t2);
+            if (x < c1) {
+                tb.off[x] = ex;
+                const uint64_t ti = (x % m) * tb.R + x / m;
+                tb.cardT[ti] = (uint32_t)v;
+                tb.offT[ti] = ex;
+                if (x + 1 == top) tb.off[top] = ex + v;
+            }
+            pre += t2;
+        }
+    }
+    if (tb.link_mode == 0) return;
+    grid_barrier(counter, target);
+    // links: row q of Z(x; tail) lies in block i (0-based tail index) with start
+    // card[x] - S_{L+i}[x] ("beginning index of Z_{>=i}"); it is
+    // incr_i of row off[y+1] - S_{L+i}[y] + k of Z(y), y = x - g_{L+i}, k = q - start.
+    const int lane = threadIdx.x & 31, t = tb.t;
+    const uint64_t gw = gt >> 5, nw = ng >> 5;
+    if (gw == 0 && lane == 0) {
+        if (tb.link_mode == 1) ((uint32_t *)tb.links)[0] = kZeroLink32;
+        else ((uint64_t *)tb.links)[0] = ~0ull;
+    }
     for (uint64_t x = 1 + gw; x < top; x += nw) {
-        const uint64_t base = __ldg(off + x);
-        const uint64_t c = __ldg(off + x + 1) - base;
-        if (c == 0) continue;
+        const uint64_t base = __ldcg(tb.off + x);
+        const uint64_t c = __ldcg(tb.off + x + 1) - base;
         for (uint64_t q = lane; q < c; q += 32) {
             int i = 0;
             uint64_t st = 0;
-            for (int j = t - 1; j >= 1; --j) {
-                uint64_t sj = c - __ldg(S + (uint64_t)(L + j) * top + x);
-                if (sj <= q) { i = j; st = sj; break; }
+            for (int jj = t - 1; jj >= 1; --jj) {
+                uint64_t sj = c - __ldcg(tb.S + (uint64_t)(L + jj) * top + x);
+                if (sj <= q) { i = jj; st = sj; break; }
             }
             const uint64_t y = x - G.g[L + i];
-            const uint64_t src = __ldg(off + y + 1) - __ldg(S + (uint64_t)(L + i) * top + y) + (q - st);
-            links[base + q] = src | ((uint64_t)i << 56);
+            const uint64_t src = __ldcg(tb.off + y + 1) - __ldcg(tb.S + (uint64_t)(L + i) * top + y) + (q - st);
+            if (tb.link_mode == 1)
+                ((uint32_t *)tb.links)[base + q] = (uint32_t)(src & tb.ring_mask) | ((uint32_t)i << kRingIdxBits);
+            else
+                ((uint64_t *)tb.links)[base + q] = src | ((uint64_t)i << 56);
         }
     }
 }
@@ -200,23 +299,140 @@ __device__ __forceinline__ void incr_word(uint32_t (&w)[T], int i)
     for (int j = 0; j < T; ++j) w[j] += (j == i) ? 1u : 0u;
 }
 
-// ---------------------------------------------------------------------- K3b
-// One CTA runs the batches in order; within a batch every row is independent
-// (elementwise x factorizationwise parallelism).  Rows of the
-// live window (the last max(tail g) x-blocks) are read from a shared-memory
-// ring when RING (fill mode 1), else from global memory written earlier by
-// this same CTA (mode 2).  The links of batch k+1 and the batch boundary of
-// batch k+2 are prefetched while batch k runs, so the per-batch critical path is
-// ring load -> increment -> ring/global store -> __syncthreads.
-template <int T, bool RING>
-__global__ void __launch_bounds__(1024) k3_fill_single(const uint64_t *__restrict__ off,
-                                                        const uint64_t *__restrict__ links, uint32_t *rows,
-                                                        uint64_t top, uint32_t b, uint64_t ring_mask)
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx_arrive(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine), completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// ---------------------------------------------------------------------- K3
+// Fill mode 1: one CTA runs the elementwise batches in order;
+// inside a batch every row is independent (factorizationwise).
+// The live window (rows of the last max(tail g) x values) sits in a shared-memory
+// ring indexed by (row & ring_mask); the u32 links (ring index of the source row |
+// incremented tail index << 27) of batch k+NS-1 are bulk-copied by the TMA engine
+// into stage (k+NS-1) % NS while batch k runs, so a batch's critical path is
+// ring load -> increment -> ring + global store -> __syncthreads.
+// Shared memory: boff[nb+1] u32 | ring[RING*T] u32 | stage[NS][SW] u32 | mbar[NS].
+template <int T>
+__global__ void __launch_bounds__(1024) k3_fill_ring(const uint64_t *__restrict__ off,
+                                                      const uint32_t *__restrict__ links, uint32_t *rows,
+                                                      uint64_t top, uint32_t b, uint32_t nb, uint32_t ring_rows,
+                                                      uint32_t stage_words)
+{
+    constexpr int NS = 8;
+    extern __shared__ __align__(16) uint32_t sh[];
+    const uint32_t ring_mask = ring_rows - 1;
+    uint32_t *boff = sh;                                            // nb + 1 entries
+    uint32_t *ring = sh + ((nb + 1 + 3) & ~3u);
+    uint32_t *stage = ring + ring_rows * T;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(stage + NS * stage_words);
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    for (uint32_t k = tid; k <= nb; k += nt) {
+        const uint64_t x = (uint64_t)k * b;
+        boff[k] = (uint32_t)__ldg(off + (x < top ? x : top));
+    }
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(mbar + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t k) {   // thread 0: bulk-copy the links of batch k
+        const uint32_t s = k % NS;
+        const uint32_t a0 = boff[k] & ~3u, a1 = (boff[k + 1] + 3u) & ~3u;
+        const uint32_t bytes = (a1 - a0) * 4u;
+        mbar_expect_tx_arrive(mbar + s, bytes);
+        if (bytes) bulk_g2s(stage + s * stage_words, links + a0, bytes, mbar + s);
+    };
+    if (tid == 0) {
+        for (uint32_t k = 0; k < NS - 1 && k < nb; ++k) issue(k);
+        mbar_wait(mbar + 0, 0);
+    }
+    __syncthreads();
+    for (uint32_t k = 0; k < nb; ++k) {
+        if (tid == 0 && k + NS - 1 < nb) issue(k + NS - 1);
+        const uint32_t R0 = boff[k], R1 = boff[k + 1];
+        const uint32_t *st = stage + (k % NS) * stage_words - (R0 & ~3u);
+        for (uint32_t r = R0 + tid; r < R1; r += nt) {
+            const uint32_t link = st[r];
+            uint32_t w[T];
+            if (link == kZeroLink32) {
+#pragma unroll
+                for (int j = 0; j < T; ++j) w[j] = 0;
+            } else {
+                const uint32_t *s = ring + (link & ((1u << kRingIdxBits) - 1)) * T;
+                if constexpr (T == 2) {
+                    uint2 v = *reinterpret_cast<const uint2 *>(s);
+                    w[0] = v.x; w[1] = v.y;
+                } else if constexpr (T == 4) {
+                    uint4 v = *reinterpret_cast<const uint4 *>(s);
+                    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < T; ++j) w[j] = s[j];
+                }
+                incr_word<T>(w, (int)(link >> kRingIdxBits));
+            }
+            uint32_t *dr = ring + (r & ring_mask) * T;
+            uint32_t *dg = rows + (uint64_t)r * T;
+            if constexpr (T == 2) {
+                *reinterpret_cast<uint2 *>(dr) = make_uint2(w[0], w[1]);
+                __stcg(reinterpret_cast<uint2 *>(dg), make_uint2(w[0], w[1]));
+            } else if constexpr (T == 4) {
+                *reinterpret_cast<uint4 *>(dr) = make_uint4(w[0], w[1], w[2], w[3]);
+                __stcg(reinterpret_cast<uint4 *>(dg), make_uint4(w[0], w[1], w[2], w[3]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < T; ++j) {
+                    dr[j] = w[j];
+                    __stcg(dg + j, w[j]);
+                }
+            }
+        }
+        if (tid == 0 && k + 1 < nb) mbar_wait(mbar + (k + 1) % NS, ((k + 1) / NS) & 1);
+        __syncthreads();
+    }
+}
+
+// Fill mode 2: one CTA, sources read back through L2 (window too large for the
+// ring, few rows per batch).  u64 links, prefetched one batch ahead.
+template <int T>
+__global__ void __launch_bounds__(1024) k3_fill_l2(const uint64_t *__restrict__ off,
+                                                    const uint64_t *__restrict__ links, uint32_t *rows,
+                                                    uint64_t top, uint32_t b)
 {
     constexpr int MAXR = 4;
-    extern __shared__ uint32_t ring[];
     const uint64_t nt = blockDim.x, tid = threadIdx.x;
-    auto bend = [&](uint64_t x0) -> uint64_t {   // off[] at the end of the batch starting at x0
+    auto bend = [&](uint64_t x0) -> uint64_t {
         uint64_t x1 = x0 + b;
         return __ldg(off + (x1 < top ? x1 : top));
     };
@@ -234,30 +450,16 @@ __global__ void __launch_bounds__(1024) k3_fill_single(const uint64_t *__restric
 #pragma unroll
             for (int j = 0; j < T; ++j) w[j] = 0;
         } else {
-            const uint64_t src = link & kLinkMask;
-            const int i = (int)(link >> 56);
-            if (RING) {
-                const uint32_t *s = ring + (src & ring_mask) * T;
+            const uint32_t *s = rows + (link & kLinkMask) * T;
 #pragma unroll
-                for (int j = 0; j < T; ++j) w[j] = s[j];
-            } else {
-                const uint32_t *s = rows + src * T;
-#pragma unroll
-                for (int j = 0; j < T; ++j) w[j] = s[j];
-            }
-            incr_word<T>(w, i);
-        }
-        if (RING) {
-            uint32_t *dr = ring + (r & ring_mask) * T;
-#pragma unroll
-            for (int j = 0; j < T; ++j) dr[j] = w[j];
+            for (int j = 0; j < T; ++j) w[j] = s[j];
+            incr_word<T>(w, (int)(link >> 56));
         }
         uint32_t *dg = rows + r * T;
 #pragma unroll
         for (int j = 0; j < T; ++j) dg[j] = w[j];
     };
     for (uint64_t x0 = 0; x0 < top; x0 += b) {
-        // prefetch: links of the next batch, boundary of the batch after it
         uint64_t nf[MAXR];
 #pragma unroll
         for (int j = 0; j < MAXR; ++j) {
@@ -280,28 +482,9 @@ __global__ void __launch_bounds__(1024) k3_fill_single(const uint64_t *__restric
     }
 }
 
-// Grid barrier for a cooperative launch (all CTAs co-resident).  `counter`
-// grows monotonically; `target` is the per-CTA running target.
-__device__ __forceinline__ void grid_barrier(unsigned int *counter, unsigned int &target)
-{
-    __syncthreads();
-    target += gridDim.x;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(counter, 1u);
-        unsigned int v;
-        while (true) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-            if ((int)(v - target) >= 0) break;
-            __nanosleep(64);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// Whole-grid variant (fill mode 3, memos with many rows per batch): the row
-// -> (x, block, source) mapping is computed inline, sources are read through L2.
+// Fill mode 3: whole grid (memos with many rows per batch); the row ->
+// (x, block, source) mapping is computed inline, sources are read through L2,
+// a grid barrier separates batches.
 template <int T>
 __global__ void __launch_bounds__(256) k3_fill_grid(Gens G, int L, uint64_t top, uint32_t b,
                                                      const uint64_t *__restrict__ S,
@@ -320,8 +503,7 @@ __global__ void __launch_bounds__(256) k3_fill_grid(Gens G, int L, uint64_t top,
 #pragma unroll
                 for (int j = 0; j < T; ++j) w[j] = 0;
             } else {
-                // x: largest x in [x0, x1) with off[x] <= r
-                uint64_t lo = x0, hi = x1 - 1;
+                uint64_t lo = x0, hi = x1 - 1;   // x: largest x in [x0, x1) with off[x] <= r
                 while (lo < hi) {
                     uint64_t mid = (lo + hi + 1) >> 1;
                     if (__ldg(off + mid) <= r) lo = mid; else hi = mid - 1;
@@ -385,24 +567,86 @@ __device__ uint64_t unrank(const uint64_t *__restrict__ Tb, uint64_t top, const 
     return R;
 }
 
-__global__ void __launch_bounds__(256) k4_plan(Gens G, PlanParams P, const uint64_t *__restrict__ S,
-                                                const uint64_t *__restrict__ W, Slice *slices, uint64_t *result)
+// floor(U * a / b) without 128-bit arithmetic (a <= b)
+__device__ __forceinline__ uint64_t mul_div(uint64_t U, uint64_t a, uint64_t b)
+{
+    return (U / b) * a + ((U % b) * a) / b;
+}
+
+// Global row index of the first row of leading prefix a (PAPER.md lex order):
+//   rank(a) = sum_j S_j[ r_{j} - (a_j + 1) g_j ],   r_0 = n, r_{j+1} = r_j - a_j g_j.
+__device__ uint64_t row_rank(const uint64_t *__restrict__ S, uint64_t top, const Gens &G, int L, uint64_t n,
+                             const uint32_t *a)
+{
+    uint64_t r = n, R = 0;
+    for (int j = 0; j < L; ++j) {
+        const uint64_t nxt = ((uint64_t)a[j] + 1) * G.g[j];
+        if (nxt <= r) R += __ldg(S + (uint64_t)j * top + (r - nxt));
+        r -= (uint64_t)a[j] * G.g[j];
+    }
+    return R;
+}
+
+// K4: shard geometry and slice table, entirely on the device (no host round trip).
+// MAT/HASH cut the rows of Z(n) evenly; COUNT cuts the leading-prefix walk evenly.
+__global__ void __launch_bounds__(256) k4_plan(Gens G, PlanArgs A, const uint64_t *__restrict__ S,
+                                                const uint64_t *__restrict__ W, PlanHdr *hdr, Slice *slices)
 {
     const int lane = threadIdx.x & 31;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    if (gw == 0 && lane < 2) result[lane] = 0;
-    const bool count_mode = (P.mode == FZ_COUNT);
-    for (uint64_t s = gw; s < P.nslices; s += nw) {
-        const uint64_t rel = s * P.slice_len;
-        const uint64_t len = (P.shard_len - rel) < P.slice_len ? (P.shard_len - rel) : P.slice_len;
+    const bool count_mode = (A.mode == FZ_COUNT);
+    const uint64_t *Tb = count_mode ? W : S;
+    const uint64_t U = __ldg(Tb + A.n);
+    const uint64_t ub = mul_div(U, A.shard, A.nshards), ue = mul_div(U, A.shard + 1, A.nshards);
+    const uint64_t len = ue - ub;
+    uint64_t slice_len = (len + A.max_slices - 1) / A.max_slices;
+    if (slice_len < A.floor_len) slice_len = A.floor_len;
+    const uint64_t nslices = (len + slice_len - 1) / slice_len;
+    if (gw == 0) {
+        uint64_t rb = ub, re = ue;
+        if (count_mode) {
+            const uint64_t rows_total = __ldg(S + A.n);
+            uint32_t a[kMaxD];
+            for (int j = 0; j < kMaxD; ++j) a[j] = 0;
+            if (ub < U) {
+                unrank(W, A.top, G, A.L, A.n, ub, a);
+                rb = row_rank(S, A.top, G, A.L, A.n, a);
+            } else {
+                rb = rows_total;
+            }
+            if (ue < U) {
+                unrank(W, A.top, G, A.L, A.n, ue, a);
+                re = row_rank(S, A.top, G, A.L, A.n, a);
+            } else {
+                re = rows_total;
+            }
+        }
+        if (lane == 0) {
+            PlanHdr h;
+            h.result[0] = 0;
+            h.result[1] = 0;
+            h.err = 0;
+            h.total_units = U;
+            h.shard_begin = ub;
+            h.shard_len = len;
+            h.slice_len = slice_len;
+            h.nslices = nslices;
+            h.row_begin = rb;
+            h.rows = re - rb;
+            *hdr = h;
+        }
+    }
+    for (uint64_t s = gw; s < nslices; s += nw) {
+        const uint64_t rel = s * slice_len;
+        const uint64_t sl_len = (len - rel) < slice_len ? (len - rel) : slice_len;
         uint32_t a[kMaxD];
         for (int j = 0; j < kMaxD; ++j) a[j] = 0;
-        const uint64_t k0 = unrank(count_mode ? W : S, P.top, G, P.L, P.n, P.shard_begin + rel, a);
+        const uint64_t k0 = unrank(Tb, A.top, G, A.L, A.n, ub + rel, a);
         if (lane == 0) {
             Slice sl;
             sl.begin = rel;
-            sl.len = len;
+            sl.len = sl_len;
             sl.k0 = count_mode ? 0 : k0;
             for (int j = 0; j < kMaxD; ++j) sl.a[j] = a[j];
             slices[s] = sl;
@@ -475,12 +719,17 @@ struct BlockInfo {      // one non-empty memo block of the current warp round (1
 
 constexpr int kWalkThreads = 256;
 
+struct WalkTables {
+    const uint32_t *cardT;   // residue-major card (w.r.t. m = g_L)
+    const uint64_t *offT;    // residue-major CSR offsets
+    const uint32_t *memo;    // CSR rows, t u32 each
+    uint64_t R;              // rows per residue column
+};
+
 template <int D, int T, int MODE>
-__global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, PlanParams P, const Slice *__restrict__ slices,
-                                                         const uint32_t *__restrict__ card,
-                                                         const uint64_t *__restrict__ off,
-                                                         const uint32_t *__restrict__ memo, uint32_t *out,
-                                                         uint64_t row_base, uint64_t *result)
+__global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
+                                                         const Slice *__restrict__ slices, WalkTables wt,
+                                                         uint32_t *out, uint64_t out_cap_rows, uint64_t row_base)
 {
     constexpr int L = D - T;
     static_assert(L >= 1, "at least one leading coordinate");
@@ -488,35 +737,57 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, PlanParams P, co
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t n = P.n;
-    const uint64_t gL = G.g[L - 1];
+    const uint32_t n = (uint32_t)n64;
+    const uint32_t m = G.g[L - 1];
+    const uint64_t nslices = hdr->nslices;
+    if (MODE == FZ_MATERIALIZE && hdr->rows > out_cap_rows) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) hdr->err = 1;
+        return;
+    }
+    if (row_base == ~0ull) row_base = hdr->row_begin;
+    uint64_t *result = hdr->result;
+    const uint32_t *__restrict__ cardT = wt.cardT;
+    const uint64_t *__restrict__ offT = wt.offT;
     uint64_t acc_rows = 0, acc_hash = 0;
     BlockInfo *bi = binfo[wib];
 
-    for (uint64_t s = gw; s < P.nslices; s += nw) {
+    for (uint64_t s = gw; s < nslices; s += nw) {
         const Slice sl = slices[s];
         uint32_t a[L];
 #pragma unroll
         for (int j = 0; j < L; ++j) a[j] = sl.a[j];
-        uint64_t r_in = n;
+        uint32_t r_in = n;
 #pragma unroll
-        for (int j = 0; j < L - 1; ++j) r_in -= (uint64_t)a[j] * G.g[j];
-        int64_t v = a[L - 1];
+        for (int j = 0; j < L - 1; ++j) r_in -= a[j] * G.g[j];
+        int32_t v = (int32_t)a[L - 1];
+        // residue-major index of p = r_in - v*m is colbase + (r_in/m - v): contiguous in v
+        uint64_t colbase = (uint64_t)(r_in % m) * wt.R + r_in / m;
         uint64_t kfirst = sl.k0;
         uint64_t left = sl.len;
         uint64_t outpos = sl.begin;
         while (left > 0) {
-            const int64_t vv = v - lane;
-            const bool valid = vv >= 0;
-            const uint64_t p = valid ? r_in - (uint64_t)vv * gL : 0;
-            uint32_t c = valid ? __ldg(card + p) : 0u;
             if constexpr (MODE == FZ_COUNT) {
-                const uint64_t nvalid = (v + 1) < 32 ? (uint64_t)(v + 1) : 32ull;
-                const uint64_t take = nvalid < left ? nvalid : left;
-                if ((uint64_t)lane < take) acc_rows += c;
+                // the run v, v-1, ..., 0 is the contiguous segment [colbase - v, colbase]
+                const uint64_t run = (uint64_t)v + 1;
+                const uint64_t take = run < left ? run : left;
+                const uint32_t *seg = cardT + (colbase - (uint64_t)v);
+                uint64_t o = 0;
+                for (; o + 128 <= take; o += 128) {
+                    const uint32_t c0 = __ldg(seg + o + lane), c1 = __ldg(seg + o + 32 + lane);
+                    const uint32_t c2 = __ldg(seg + o + 64 + lane), c3 = __ldg(seg + o + 96 + lane);
+                    acc_rows += (uint64_t)c0 + c1 + c2 + c3;
+                }
+                for (; o < take; o += 32)
+                    if (o + lane < take) acc_rows += __ldg(seg + o + lane);
                 left -= take;
+                if (left == 0) break;
+                v = -1;
             } else {
-                uint64_t mrow = valid ? __ldg(off + p) : 0;
+                const int32_t vv = v - lane;
+                const bool valid = vv >= 0;
+                const uint64_t ti = colbase - (uint64_t)v + lane;
+                uint32_t c = valid ? __ldg(cardT + ti) : 0u;
+                uint64_t mrow = valid ? __ldg(offT + ti) : 0;
                 if (lane == 0) {
                     c -= (uint32_t)kfirst;
                     mrow += kfirst;
@@ -556,7 +827,7 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, PlanParams P, co
                         w[L - 1] = info.v;
                         if constexpr (T > 0) {
                             uint32_t tw[T];
-                            load_tail<T>(memo + (info.memo_row + (q - info.start)) * T, tw);
+                            load_tail<T>(wt.memo + (info.memo_row + (q - info.start)) * T, tw);
 #pragma unroll
                             for (int j = 0; j < T; ++j) w[L + j] = tw[j];
                         }
@@ -572,11 +843,11 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, PlanParams P, co
                 acc_rows += (lane == 0) ? use : 0;
                 outpos += use;
                 left -= use;
-            }
-            if (left == 0) break;
-            if (v >= 32) {
-                v -= 32;
-                continue;
+                if (left == 0) break;
+                if (v >= 32) {
+                    v -= 32;
+                    continue;
+                }
             }
             // carry: nextCandidate over the outer leading coordinates:
             // rightmost nonzero index i < L-1, a_i--, later coordinates restart at their maximum.
@@ -585,22 +856,29 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, PlanParams P, co
             for (int j = 0; j < L - 1; ++j)
                 if (a[j] > 0) i = j;
             if (i < 0) break;   // end of stream
-            uint64_t r = n;
+            if (i == L - 2) {   // common case: only a_{L-1} changes, r_in grows by g_{L-1}
+                a[L - 2] -= 1;
+                r_in += G.g[L - 2];
+            } else {
+                uint32_t r = n;
 #pragma unroll
-            for (int j = 0; j < L - 1; ++j) {
-                if (j == i) a[j] -= 1;
-                if (j > i) a[j] = (uint32_t)(r / G.g[j]);
-                r -= (uint64_t)a[j] * G.g[j];
+                for (int j = 0; j < L - 1; ++j) {
+                    if (j == i) a[j] -= 1;
+                    if (j > i) a[j] = r / G.g[j];
+                    r -= a[j] * G.g[j];
+                }
+                r_in = r;
             }
-            r_in = r;
-            v = (int64_t)(r / gL);
+            const uint32_t q = r_in / m;
+            v = (int32_t)q;
+            colbase = (uint64_t)(r_in - q * m) * wt.R + q;
         }
     }
     acc_rows = warp_sum_u64(acc_rows);
-    acc_hash = warp_sum_u64(acc_hash);
-    if (lane == 0) {
-        atomicAdd((unsigned long long *)result, (unsigned long long)acc_rows);
-        if (MODE == FZ_HASH) atomicAdd((unsigned long long *)(result + 1), (unsigned long long)acc_hash);
+    if (lane == 0) atomicAdd((unsigned long long *)result, (unsigned long long)acc_rows);
+    if constexpr (MODE == FZ_HASH) {
+        acc_hash = warp_sum_u64(acc_hash);
+        if (lane == 0) atomicAdd((unsigned long long *)(result + 1), (unsigned long long)acc_hash);
     }
 }
 

