@@ -65,7 +65,9 @@ typedef struct {
     uint64_t max_card;      /* max_x |Z(x; tail)| */
     uint64_t batches;       /* elementwise batches of the copy-increment pass */
     uint32_t batch;         /* batch size b = min(tail g) */
-    int fill_mode;          /* 0 = no rows, 1 = single-CTA shared-memory ring, 2 = single CTA via L2, 3 = whole grid */
+    int fill_mode;          /* 0 = no rows; 1 = one CTA, batches of min(tail g), shared-memory ring;
+                               2 = same through L2; 3 = whole grid, batches of min(tail g);
+                               4 = one pass per tail dimension, one warp per residue chain */
     uint64_t window_rows;   /* max rows a batch and its look-back window span (ring size needed) */
 } fz_memo_info;
 
@@ -81,6 +83,10 @@ fz_status fz_memo_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t t
 
 /* Memory cap for memo rows (bytes); 0 restores the default 8e9. */
 void fz_set_memo_cap(uint64_t bytes);
+
+/* Force the copy-increment schedule of later layouts (1..4, see fz_memo_info.fill_mode;
+ * a mode that does not fit falls back to the automatic choice); 0 = automatic. */
+void fz_set_fill_mode(int mode);
 
 /* A1 as a reusable host object (like an FFT plan): validation, sizing and the
  * host copy of the count tables for (gens, d, t, top, with_entries).  Building

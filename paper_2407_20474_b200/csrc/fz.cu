@@ -26,6 +26,7 @@ namespace {
 thread_local std::string g_err;
 thread_local uint64_t g_launches = 0;
 uint64_t g_memo_cap = 8000000000ull;
+int g_fill_override = 0;               // 0 = automatic fill-mode choice
 
 fz_status fail(fz_status st, const char *fmt, ...)
 {
@@ -116,14 +117,17 @@ struct Sizing {
     uint64_t top;
     uint64_t entries = 0, max_card = 0, window = 0, ring_rows = 0, batches = 0;
     uint32_t batch = 0;
-    uint32_t stage_words = 0;   // fill mode 1: words per TMA link stage
+    uint32_t stage_words = 0;   // fill mode 1: words per TMA link chunk buffer
+    uint32_t chb = 0;           // fill mode 1: batches per link chunk
+    uint32_t Q = 1;             // fill mode 1: batches the bulk stores may lag behind
+    uint64_t max_batch_rows = 0;
+    uint64_t level_block[FZ_MAX_D] = {0};   // fill mode 4: largest block i of any Z(x), per tail level
     uint64_t smem_bytes = 0;    // fill mode 1: dynamic shared memory
     int fill_mode = 0;
     Layout lay{};
 };
 
 constexpr uint64_t kSmemMax = 220 * 1024;   // dynamic shared memory budget of the ring fill
-constexpr int kRingStages = 8;              // must match k3_fill_ring's NS
 constexpr int kMaxGrid = 1024;              // chunk scratch entries of the K1 grid
 
 fz_status validate(const uint32_t *g, int d, int t, uint64_t top)
@@ -177,23 +181,63 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
             return fail(FZ_ECAP, "memo of %llu rows x %d coords exceeds the cap of %llu bytes",
                         (unsigned long long)entries, t, (unsigned long long)g_memo_cap);
         rows_bytes = entries * 4ull * t;
-        uint64_t ring = 4;
-        while (ring < win) ring <<= 1;
-        z.ring_rows = ring;
-        // mode 1 needs u32 CSR rows, the ring, NS link stages and the batch offsets in shared memory
-        uint64_t sw = 0;
-        for (uint64_t k = 0; k < z.batches; ++k) {
-            uint64_t x0 = k * b, x1 = std::min<uint64_t>(x0 + b, top);
-            uint64_t a0 = off[x0] & ~3ull, a1 = (off[x1] + 3) & ~3ull;
-            sw = std::max(sw, a1 - a0);
+        // fill mode 1 (k3_fill_ring): ring over the rows of [x0 - max(hmax, 2b), x0 + b) for every batch
+        // (look-back window + the batch whose bulk store may still be reading), links in chunks of chb batches
+        // ring: rows of [x0 - max(hmax, (Q+1) b), x0 + b) for every batch (look-back window + batches whose
+        // bulk store may still be pending); links in chunks of chb batches.  Largest Q, chb that fit.
+        auto boffv = [&](uint64_t k) { return off[std::min<uint64_t>(k * b, top)]; };
+        auto ring_for = [&](uint64_t Q) {
+            uint64_t win2 = 0;
+            const uint64_t back = std::max<uint64_t>((uint64_t)hmax, (Q + 1) * b);
+            for (uint64_t x0 = 0; x0 < top; x0 += b) {
+                uint64_t lo = x0 > back ? x0 - back : 0, hi = std::min<uint64_t>(x0 + b, top);
+                win2 = std::max<uint64_t>(win2, off[hi] - off[lo]);
+            }
+            uint64_t ring = 4;
+            while (ring < win2 + 4) ring <<= 1;   // + the rows sharing the first 16-B granule of a bulk store
+            return ring;
+        };
+        auto chunk_for = [&](uint64_t chb) {
+            uint64_t cw = 0;
+            for (uint64_t k0 = 0; k0 < z.batches; k0 += chb) {
+                uint64_t k1 = std::min<uint64_t>(k0 + chb, z.batches);
+                cw = std::max<uint64_t>(cw, ((boffv(k1) + 3) & ~3ull) - (boffv(k0) & ~3ull));
+            }
+            return cw;
+        };
+        uint64_t smem = ~0ull, chb = 2, cw = 0, ring = 0, Q = 1;
+        bool fit = false;
+        for (uint64_t q : {8ull, 4ull, 2ull, 1ull}) {
+            ring = ring_for(q);
+            for (uint64_t cb : {32ull, 16ull, 8ull, 4ull, 2ull}) {
+                cw = chunk_for(cb);
+                smem = 4 * ((z.batches + 1 + 3) & ~3ull) + ring * 4ull * t + 2 * 4ull * cw + 32;
+                if (smem <= kSmemMax) { chb = cb; Q = q; fit = true; break; }
+            }
+            if (fit) break;
         }
-        z.stage_words = (uint32_t)std::min<uint64_t>(sw, 0xffffffffu);
-        const uint64_t smem = 4 * ((z.batches + 1 + 3) & ~3ull) + ring * 4ull * t + kRingStages * 4ull * sw +
-                              8ull * kRingStages;
+        z.ring_rows = ring;
+        z.Q = (uint32_t)Q;
+        for (uint64_t k = 0; k < z.batches; ++k) z.max_batch_rows = std::max<uint64_t>(z.max_batch_rows, boffv(k + 1) - boffv(k));
+        z.chb = (uint32_t)std::max<uint64_t>(chb, 1);
+        z.stage_words = (uint32_t)std::min<uint64_t>(cw, 0xffffffffu);
         z.smem_bytes = smem;
-        if (entries >= (1ull << 25) || entries / z.batches > 16384)
+        bool chains_fit = true;
+        for (int i = 0; i + 1 < t; ++i) {
+            const uint64_t *Si = H.S.data() + (size_t)(L + i) * top, *Si1 = Si + top;
+            uint64_t mb = 0;
+            for (uint64_t x = 0; x < top; ++x) mb = std::max<uint64_t>(mb, Si[x] - Si1[x]);
+            z.level_block[i] = mb;
+            if (mb > 128 && 2ull * 256 * 4 * t + mb * 4ull * t > kSmemMax) chains_fit = false;
+        }
+        const int forced = g_fill_override;
+        if (forced >= 1 && forced <= 4 && !(forced == 1 && !fit) && !(forced == 4 && !chains_fit))
+            z.fill_mode = forced;
+        else if (entries >= (1ull << 25) || entries / z.batches > 16384)
             z.fill_mode = 3;
-        else if (smem <= kSmemMax && entries < (1ull << 31) && ring < (1ull << 27))
+        else if (chains_fit)
+            z.fill_mode = 4;
+        else if (fit && entries < (1ull << 31) && ring < (1ull << 27))
             z.fill_mode = 1;
         else
             z.fill_mode = 2;
@@ -275,10 +319,38 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
     if (z.fill_mode == 1) {
         const size_t smem = (size_t)z.smem_bytes;
         FZ_CUDA(cudaFuncSetAttribute(fzk::k3_fill_ring<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        fzk::k3_fill_ring<T><<<1, 1024, smem, s>>>(m->off, (const uint32_t *)m->links, m->rows, z.top, z.batch,
-                                                   (uint32_t)z.batches, (uint32_t)z.ring_rows, z.stage_words);
+        // workers: enough that the largest batch needs <= 4 rows per thread (prefetched in registers)
+        const unsigned workers =
+            (unsigned)std::min<uint64_t>(992, std::max<uint64_t>(64, align_up((z.max_batch_rows + 3) / 4, 32)));
+        fzk::k3_fill_ring<T><<<1, workers + 32, smem, s>>>(m->off, (const uint32_t *)m->links, m->rows, z.top, z.batch,
+                                                   (uint32_t)z.batches, (uint32_t)z.ring_rows, z.stage_words, z.chb, z.Q);
         ++g_launches;
         return cuda_check("k3_fill_ring");
+    }
+    if (z.fill_mode == 4) {
+        const uint32_t h_last = m->lay->g[z.d - 1];
+        const unsigned blocks = (unsigned)std::min<uint64_t>((z.top + 255) / 256, (uint64_t)device_sms() * 8);
+        fzk::k3_last_level<T><<<std::max(blocks, 1u), 256, 0, s>>>(m->S, m->off, m->rows, z.top, z.L, h_last);
+        ++g_launches;
+        fz_status st = cuda_check("k3_last_level");
+        for (int i = T - 2; i >= 0 && !st; --i) {
+            const uint32_t h = m->lay->g[z.L + i];
+            const uint64_t mb = z.level_block[i];
+            const unsigned chains = (unsigned)std::min<uint64_t>(h, z.top);
+            const size_t stage = 2ull * fzk::kChainStage * T * 4;
+            if (mb <= 32) fzk::k3_chain<T, 1><<<chains, 32, stage, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
+            else if (mb <= 64) fzk::k3_chain<T, 2><<<chains, 32, stage, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
+            else if (mb <= 96) fzk::k3_chain<T, 3><<<chains, 32, stage, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
+            else if (mb <= 128) fzk::k3_chain<T, 4><<<chains, 32, stage, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
+            else {
+                const size_t smem = stage + mb * 4ull * T;
+                FZ_CUDA(cudaFuncSetAttribute(fzk::k3_chain<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                fzk::k3_chain<T, 0><<<chains, 32, smem, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
+            }
+            ++g_launches;
+            st = cuda_check("k3_chain");
+        }
+        return st;
     }
     if (z.fill_mode == 2) {
         fzk::k3_fill_l2<T><<<1, 1024, 0, s>>>(m->off, (const uint64_t *)m->links, m->rows, z.top, z.batch);
@@ -445,6 +517,7 @@ extern "C" {
 const char *fz_last_error(void) { return g_err.c_str(); }
 uint64_t fz_launch_count(void) { return g_launches; }
 void fz_set_memo_cap(uint64_t bytes) { g_memo_cap = bytes ? bytes : 8000000000ull; }
+void fz_set_fill_mode(int mode) { g_fill_override = (mode >= 1 && mode <= 4) ? mode : 0; }
 
 fz_status fz_layout_create(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out)
 {

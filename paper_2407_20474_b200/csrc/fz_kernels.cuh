@@ -335,55 +335,163 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 // ---------------------------------------------------------------------- K3
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t nthreads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+
 // Fill mode 1: one CTA runs the elementwise batches in order;
 // inside a batch every row is independent (factorizationwise).
-// The live window (rows of the last max(tail g) x values) sits in a shared-memory
-// ring indexed by (row & ring_mask); the u32 links (ring index of the source row |
-// incremented tail index << 27) of batch k+NS-1 are bulk-copied by the TMA engine
-// into stage (k+NS-1) % NS while batch k runs, so a batch's critical path is
-// ring load -> increment -> ring + global store -> __syncthreads.
-// Shared memory: boff[nb+1] u32 | ring[RING*T] u32 | stage[NS][SW] u32 | mbar[NS].
+// Worker warps compute rows only in shared memory: the live window sits in a
+// ring indexed by (row & mask); a row is ring[src] with one coordinate
+// incremented, src / index from the u32 link (ring index | tail index << 27).
+// Workers prefetch the next batch's links into registers, so a batch's
+// dependent chain is ring LDS -> increment -> ring STS -> named barrier.
+// The last warp is a TMA helper that never joins the workers' barrier: it
+// bulk-loads the links CHB batches at a time (double-buffered, mbarrier
+// completion) and bulk-stores finished batches from the ring to the global CSR,
+// following the workers through a release/acquire progress counter; workers only
+// wait for it when the ring would overwrite rows not yet stored (Q batches back).
+// Shared memory: boff[nb+1] u32 | ring[RING*T] u32 | lbuf[2][chunk_words] u32 |
+//                mbar[2] | done, stored (u32).
 template <int T>
 __global__ void __launch_bounds__(1024) k3_fill_ring(const uint64_t *__restrict__ off,
                                                       const uint32_t *__restrict__ links, uint32_t *rows,
                                                       uint64_t top, uint32_t b, uint32_t nb, uint32_t ring_rows,
-                                                      uint32_t stage_words)
+                                                      uint32_t chunk_words, uint32_t chb, uint32_t Q)
 {
-    constexpr int NS = 8;
+    constexpr int RPT = 4;
     extern __shared__ __align__(16) uint32_t sh[];
     const uint32_t ring_mask = ring_rows - 1;
     uint32_t *boff = sh;                                            // nb + 1 entries
     uint32_t *ring = sh + ((nb + 1 + 3) & ~3u);
-    uint32_t *stage = ring + ring_rows * T;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(stage + NS * stage_words);
-    const uint32_t tid = threadIdx.x, nt = blockDim.x;
-    for (uint32_t k = tid; k <= nb; k += nt) {
+    uint32_t *lbuf = ring + ring_rows * T;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(lbuf + 2 * chunk_words);
+    uint32_t *done = reinterpret_cast<uint32_t *>(mbar + 2);
+    uint32_t *stored = done + 1;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t nw = blockDim.x - 32;                           // worker threads
+    const bool helper = tid >= nw;
+    const uint32_t nchunks = (nb + chb - 1) / chb;
+    const uint64_t ring_bytes = (uint64_t)ring_rows * T * 4;
+    for (uint32_t k = tid; k <= nb; k += blockDim.x) {
         const uint64_t x = (uint64_t)k * b;
         boff[k] = (uint32_t)__ldg(off + (x < top ? x : top));
     }
     if (tid == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(mbar + s, 1);
+        mbar_init(mbar + 0, 1);
+        mbar_init(mbar + 1, 1);
+        *done = 0;
+        *stored = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    auto issue = [&](uint32_t k) {   // thread 0: bulk-copy the links of batch k
-        const uint32_t s = k % NS;
-        const uint32_t a0 = boff[k] & ~3u, a1 = (boff[k + 1] + 3u) & ~3u;
-        const uint32_t bytes = (a1 - a0) * 4u;
-        mbar_expect_tx_arrive(mbar + s, bytes);
-        if (bytes) bulk_g2s(stage + s * stage_words, links + a0, bytes, mbar + s);
-    };
-    if (tid == 0) {
-        for (uint32_t k = 0; k < NS - 1 && k < nb; ++k) issue(k);
-        mbar_wait(mbar + 0, 0);
+    auto chunk_base = [&](uint32_t c) { return boff[c * chb] & ~3u; };
+
+    if (helper) {
+        if ((tid & 31) != 0) return;
+        auto load_chunk = [&](uint32_t c) {
+            const uint32_t k1 = (c + 1) * chb < nb ? (c + 1) * chb : nb;
+            const uint32_t a0 = chunk_base(c), a1 = (boff[k1] + 3u) & ~3u;
+            const uint32_t bytes = (a1 - a0) * 4u;
+            fence_proxy_async();
+            mbar_expect_tx_arrive(mbar + (c & 1), bytes);
+            if (bytes) bulk_g2s(lbuf + (c & 1) * chunk_words, links + a0, bytes, mbar + (c & 1));
+        };
+        // bytes [B0, B1) of the CSR rows <- ring bytes B0 mod ring_bytes (split at the wrap)
+        auto store_bytes = [&](uint64_t B0, uint64_t B1) {
+            while (B0 < B1) {
+                const uint64_t rb = B0 % ring_bytes;
+                uint64_t len = B1 - B0;
+                if (rb + len > ring_bytes) len = ring_bytes - rb;
+                bulk_s2g(reinterpret_cast<char *>(rows) + B0, reinterpret_cast<char *>(ring) + rb, (uint32_t)len);
+                B0 += len;
+            }
+        };
+        load_chunk(0);
+        uint32_t next_chunk = 1, j = 0;
+        while (j < nb) {
+            const uint32_t d = ld_acquire_cta(done);
+            if (next_chunk < nchunks && d >= (next_chunk - 1) * chb) {   // workers are in chunk next_chunk-1
+                load_chunk(next_chunk);
+                ++next_chunk;
+            }
+            if (d > j) {
+                fence_proxy_async();
+                const uint64_t B0 = ((uint64_t)boff[j] * T * 4) & ~15ull;
+                uint64_t B1 = (uint64_t)boff[d] * T * 4;
+                B1 = (d == nb) ? ((B1 + 15) & ~15ull) : (B1 & ~15ull);
+                store_bytes(B0, B1);
+                bulk_commit();
+                bulk_wait_read<0>();
+                st_release_cta(stored, d);
+                j = d;
+            } else {
+                __nanosleep(20);
+            }
+        }
+        bulk_wait_all();
+        return;
     }
-    __syncthreads();
+
+    // ------------------------------------------------------------- workers
+    auto wait_chunk = [&](uint32_t c) { mbar_wait(mbar + (c & 1), (c >> 1) & 1); };
+    wait_chunk(0);
+    uint32_t lnk[RPT];
+    uint32_t R0 = boff[0], R1 = boff[1];
+    const uint32_t *lk = lbuf - chunk_base(0);
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const uint32_t r = R0 + tid + q * nw;
+        lnk[q] = r < R1 ? lk[r] : 0u;
+    }
+    uint32_t c = 0, kk = 0;
     for (uint32_t k = 0; k < nb; ++k) {
-        if (tid == 0 && k + NS - 1 < nb) issue(k + NS - 1);
-        const uint32_t R0 = boff[k], R1 = boff[k + 1];
-        const uint32_t *st = stage + (k % NS) * stage_words - (R0 & ~3u);
-        for (uint32_t r = R0 + tid; r < R1; r += nt) {
-            const uint32_t link = st[r];
+        // ring-reuse guard: the ring holds batches k-Q-1..k (+ one 16-B granule), so batch k may only
+        // overwrite rows once every batch before k-Q-1 has been read by its bulk store
+        if (tid == 0 && k > Q + 1) {
+            while (ld_acquire_cta(stored) + Q + 1 < k) __nanosleep(20);
+        }
+        if (k > 0) named_bar(1, nw);
+        if (tid == 0 && k > 0) st_release_cta(done, k);
+        // next batch's boundaries and links (independent of this batch's results)
+        const uint32_t Rn = R1, Rn1 = (k + 1 < nb) ? boff[k + 2] : R1;
+        uint32_t kk1 = kk + 1, c1 = c;
+        if (kk1 == chb) {
+            kk1 = 0;
+            ++c1;
+            if (c1 < nchunks) wait_chunk(c1);
+        }
+        const uint32_t *lk1 = (c1 == c) ? lk : lbuf + (c1 & 1) * chunk_words - chunk_base(c1 < nchunks ? c1 : 0);
+        uint32_t nl[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const uint32_t r = Rn + tid + q * nw;
+            nl[q] = r < Rn1 ? lk1[r] : 0u;
+        }
+        auto row = [&](uint32_t r, uint32_t link) {
             uint32_t w[T];
             if (link == kZeroLink32) {
 #pragma unroll
@@ -403,23 +511,219 @@ __global__ void __launch_bounds__(1024) k3_fill_ring(const uint64_t *__restrict_
                 incr_word<T>(w, (int)(link >> kRingIdxBits));
             }
             uint32_t *dr = ring + (r & ring_mask) * T;
-            uint32_t *dg = rows + (uint64_t)r * T;
             if constexpr (T == 2) {
                 *reinterpret_cast<uint2 *>(dr) = make_uint2(w[0], w[1]);
-                __stcg(reinterpret_cast<uint2 *>(dg), make_uint2(w[0], w[1]));
             } else if constexpr (T == 4) {
                 *reinterpret_cast<uint4 *>(dr) = make_uint4(w[0], w[1], w[2], w[3]);
-                __stcg(reinterpret_cast<uint4 *>(dg), make_uint4(w[0], w[1], w[2], w[3]));
             } else {
 #pragma unroll
-                for (int j = 0; j < T; ++j) {
-                    dr[j] = w[j];
-                    __stcg(dg + j, w[j]);
+                for (int j = 0; j < T; ++j) dr[j] = w[j];
+            }
+        };
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const uint32_t r = R0 + tid + q * nw;
+            if (r < R1) row(r, lnk[q]);
+        }
+        for (uint32_t r = R0 + tid + RPT * nw; r < R1; r += nw) row(r, lk[r]);   // rare: oversized batch
+        R0 = Rn;
+        R1 = Rn1;
+        kk = kk1;
+        c = c1;
+        lk = lk1;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) lnk[q] = nl[q];
+    }
+    named_bar(1, nw);
+    if (tid == 0) st_release_cta(done, nb);
+}
+
+// ------------------------------------------------------------- K3 chains
+// Fill mode 4 (default): the same copy-increment tasks as PAPER.md:171-192,
+// scheduled one tail dimension at a time.  With tail index i (0-based) and
+// h = h_i, block i of Z(x) is
+//     incr_i( Z_{>=i}(x - h) ) = incr_i( block_i(Z(x - h)) ++ Z_{>=i+1}(x - h) )
+// (PAPER.md:77-88 with PAPER.md:83-85), so once blocks i+1.. exist (earlier
+// passes), block i only depends on block i of x - h: the x values of one
+// residue class r mod h form an independent chain, and the elementwise batch of
+// pass i is {one x per residue} (size h_i >= min h).  Each
+// chain is one warp; the block state lives in registers (K slots of 32 rows) or in
+// shared memory (K = 0), each step adds 1 to coordinate i of every row and appends
+// the suffix Z_{>=i+1}(x - h) (incremented), then stores the block.  No CTA or
+// grid barrier inside a pass.  Per 32-step group the lanes prefetch the step
+// metadata from the count tables and stage the suffix rows in shared memory with
+// cp.async.
+
+// last tail dimension: block t-1 of Z(x) = [(0,..,0, x/h)] if h | x (x = 0 gives Memo[0] = [0])
+template <int T>
+__global__ void __launch_bounds__(256) k3_last_level(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                                      uint32_t *rows, uint64_t top, int L, uint32_t h)
+{
+    const uint64_t *Sl = S + (uint64_t)(L + T - 1) * top;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < top; x += (uint64_t)gridDim.x * blockDim.x) {
+        if (x % h) continue;
+        const uint64_t dst = __ldg(off + x + 1) - __ldg(Sl + x);
+        uint32_t *o = rows + dst * T;
+#pragma unroll
+        for (int j = 0; j < T - 1; ++j) o[j] = 0;
+        o[T - 1] = (uint32_t)(x / h);
+    }
+}
+
+__device__ __forceinline__ void cp_async4(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+constexpr int kChainStage = 256;   // staged suffix rows per 32-step group
+
+// K > 0: block rows in registers, row q at lane q % 32, slot q / 32 (block <= 32 K rows).
+// K = 0: block rows in dynamic shared memory (cap rows).
+template <int T, int K>
+__global__ void __launch_bounds__(32) k3_chain(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                                uint32_t *rows, uint64_t top, int L, int i, uint32_t h)
+{
+    extern __shared__ __align__(16) uint32_t csh[];
+    uint32_t *stage = csh;                               // [2][kChainStage * T]
+    uint32_t *blk = csh + 2 * kChainStage * T;          // K == 0: block rows
+    const int lane = threadIdx.x;
+    const uint64_t r = blockIdx.x;
+    if (r + h >= top) return;
+    const uint64_t *Si = S + (uint64_t)(L + i) * top;
+    const uint64_t *Si1 = S + (uint64_t)(L + i + 1) * top;
+    const uint64_t nsteps = (top - 1 - r) / h;          // x = r + s h, s < nsteps, has x + h < top
+    uint32_t inc[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) inc[j] = (j == i) ? 1u : 0u;
+    uint32_t st[K > 0 ? K : 1][T];
+#pragma unroll
+    for (int k = 0; k < (K > 0 ? K : 1); ++k)
+#pragma unroll
+        for (int j = 0; j < T; ++j) st[k][j] = 0;
+    uint32_t n = 0;                                      // rows of block i of Z(x)
+
+    // metadata of step s = 32 g + lane: suffix length / start of Z(x), block start of Z(x + h)
+    auto meta = [&](uint64_t g, uint32_t &ns, uint64_t &so, uint64_t &dst) {
+        const uint64_t s = g * 32 + lane;
+        ns = 0; so = 0; dst = 0;
+        if (s < nsteps) {
+            const uint64_t x = r + s * h, xn = x + h;
+            ns = (uint32_t)__ldg(Si1 + x);
+            so = __ldg(off + x + 1) - ns;
+            dst = __ldg(off + xn + 1) - __ldg(Si + xn);
+        }
+    };
+    // stage the suffix rows of group g into buffer b (excl = row position of this lane's step)
+    auto stage_group = [&](uint32_t ns, uint64_t so, uint32_t excl, int b) {
+        uint32_t *sb = stage + b * kChainStage * T;
+        for (int l = 0; l < 32; ++l) {
+            const uint32_t nl = __shfl_sync(kFull, ns, l);
+            if (nl == 0) continue;
+            const uint32_t el = __shfl_sync(kFull, excl, l);
+            const uint64_t sl = shfl_u64(so, l);
+            for (uint32_t j = lane; j < nl && el + j < (uint32_t)kChainStage; j += 32)
+#pragma unroll
+                for (int w = 0; w < T; ++w) cp_async4(sb + (el + j) * T + w, rows + (sl + j) * T + w);
+        }
+        cp_async_commit();
+    };
+    auto scan = [&](uint32_t v) {
+        uint32_t inc2 = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t u = __shfl_up_sync(kFull, inc2, o);
+            if (lane >= o) inc2 += u;
+        }
+        return inc2 - v;
+    };
+    // one chain step: block of Z(x + h) = incr_i(block of Z(x) ++ suffix rows of Z(x))
+    auto step = [&](const uint32_t *sb, uint32_t ns, uint32_t ex, uint64_t so, uint64_t dst) {
+        auto srow = [&](uint32_t j, int q) -> uint32_t {
+            return (ex + j < (uint32_t)kChainStage) ? sb[(ex + j) * T + q] : rows[(so + j) * T + q];
+        };
+        if constexpr (K > 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int j = 0; j < T; ++j) st[k][j] += inc[j];
+            for (uint32_t j0 = 0; j0 < ns; j0 += 32) {
+                const uint32_t base = n + j0;
+                const uint32_t jj = (uint32_t)(lane - (int)base) & 31u;   // suffix row landing on this lane
+                const uint32_t js = j0 + jj;
+                if (js < ns) {
+                    uint32_t w[T];
+#pragma unroll
+                    for (int q = 0; q < T; ++q) w[q] = srow(js, q) + inc[q];
+                    const uint32_t slot = (base + jj) >> 5;
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if (k == (int)slot)
+#pragma unroll
+                            for (int q = 0; q < T; ++q) st[k][q] = w[q];
                 }
             }
+            n += ns;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const uint32_t q = lane + 32 * k;
+                if (q < n) {
+                    uint32_t *o = rows + (dst + q) * T;
+#pragma unroll
+                    for (int j = 0; j < T; ++j) o[j] = st[k][j];
+                }
+            }
+        } else {
+            for (uint32_t q = lane; q < n; q += 32) {
+                uint32_t *bq = blk + q * T;
+                uint32_t *o = rows + (dst + q) * T;
+#pragma unroll
+                for (int j = 0; j < T; ++j) {
+                    const uint32_t v = bq[j] + inc[j];
+                    bq[j] = v;
+                    o[j] = v;
+                }
+            }
+            for (uint32_t j = lane; j < ns; j += 32) {
+                uint32_t *bq = blk + (n + j) * T;
+                uint32_t *o = rows + (dst + n + j) * T;
+#pragma unroll
+                for (int q = 0; q < T; ++q) {
+                    const uint32_t v = srow(j, q) + inc[q];
+                    bq[q] = v;
+                    o[q] = v;
+                }
+            }
+            n += ns;
+            __syncwarp();
         }
-        if (tid == 0 && k + 1 < nb) mbar_wait(mbar + (k + 1) % NS, ((k + 1) / NS) & 1);
-        __syncthreads();
+    };
+    uint32_t c_ns, n_ns = 0, n_ex = 0;
+    uint64_t c_so, c_dst, n_so = 0, n_dst = 0;
+    meta(0, c_ns, c_so, c_dst);
+    uint32_t c_ex = scan(c_ns);
+    stage_group(c_ns, c_so, c_ex, 0);
+    const uint64_t ngroups = (nsteps + 31) / 32;
+    for (uint64_t g = 0; g < ngroups; ++g) {
+        const int b = (int)(g & 1);
+        const bool more = g + 1 < ngroups;
+        if (more) {
+            meta(g + 1, n_ns, n_so, n_dst);
+            n_ex = scan(n_ns);
+        }
+        cp_async_wait_all();   // group g is staged
+        __syncwarp();
+        if (more) stage_group(n_ns, n_so, n_ex, b ^ 1);   // buffer b^1 held group g-1 (done)
+        const uint32_t *sb = stage + b * kChainStage * T;
+        const uint32_t steps = (uint32_t)((nsteps - g * 32) < 32 ? (nsteps - g * 32) : 32);
+        for (uint32_t l = 0; l < steps; ++l)
+            step(sb, __shfl_sync(kFull, c_ns, l), __shfl_sync(kFull, c_ex, l), shfl_u64(c_so, l), shfl_u64(c_dst, l));
+        c_ns = n_ns;
+        c_so = n_so;
+        c_dst = n_dst;
+        c_ex = n_ex;
+        __syncwarp();
     }
 }
 

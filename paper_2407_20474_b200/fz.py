@@ -74,6 +74,8 @@ def _load():
     L.fz_launch_count.restype = ctypes.c_uint64
     L.fz_set_memo_cap.argtypes = [u64]
     L.fz_set_memo_cap.restype = None
+    L.fz_set_fill_mode.argtypes = [c_int]
+    L.fz_set_fill_mode.restype = None
     return L
 
 
@@ -108,6 +110,11 @@ def set_memo_cap(nbytes: int) -> None:
     _L.fz_set_memo_cap(nbytes)
 
 
+def set_fill_mode(mode: int) -> None:
+    """Force the memo copy-increment schedule (1 ring, 2 L2, 3 grid, 4 chains; 0 = automatic)."""
+    _L.fz_set_fill_mode(int(mode))
+
+
 class Layout:
     """A1 host object (fz_layout): validation, sizing and host tables for (gens, t, top)."""
 
@@ -126,7 +133,7 @@ class Layout:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _L is not None:
             _L.fz_layout_free(h)
             self.h = None
 
@@ -153,7 +160,7 @@ class Memo:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _L is not None:
             _L.fz_free(h)
             self.h = None
 
@@ -235,7 +242,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _L is not None:
             _L.fz_plan_free(h)
             self.h = None
 
