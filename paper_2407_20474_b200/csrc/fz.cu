@@ -308,7 +308,7 @@ uint64_t max_slices()
     return (uint64_t)device_sms() * 8 * (fzk::kWalkThreads / 32) * 4;
 }
 
-uint64_t plan_bytes() { return kPlanHeader + align_up(max_slices() * sizeof(Slice), 256); }
+uint64_t plan_bytes() { return kPlanHeader; }   // the header; slices are unranked inside K5
 
 unsigned walk_blocks() { return (unsigned)device_sms() * 8; }
 
@@ -394,7 +394,8 @@ struct WalkArgs {
     Gens G;
     uint64_t n;
     PlanHdr *hdr;
-    const Slice *slices;
+    const uint64_t *Tb;
+    uint64_t top;
     fzk::WalkTables wt;
     uint32_t *out;
     uint64_t cap;
@@ -404,7 +405,7 @@ struct WalkArgs {
 template <int D, int T, int MODE>
 fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
 {
-    fzk::k5_walk<D, T, MODE><<<walk_blocks(), fzk::kWalkThreads, 0, s>>>(a.G, a.n, a.hdr, a.slices, a.wt, a.out,
+    fzk::k5_walk<D, T, MODE><<<walk_blocks(), fzk::kWalkThreads, 0, s>>>(a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out,
                                                                          a.cap, a.row_base);
     ++g_launches;
     return cuda_check("k5_walk");
@@ -721,9 +722,7 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
     A.nshards = nshards;
     A.L = z.L;
     Gens G = make_gens(m->lay->g, z.d);
-    const unsigned blocks = (unsigned)std::min<uint64_t>((A.max_slices * 32 + 255) / 256, 4096);
-    fzk::k4_plan<<<blocks, 256, 0, (cudaStream_t)stream>>>(G, A, m->S, m->W, (PlanHdr *)p->d_plan,
-                                                           (Slice *)(p->d_plan + kPlanHeader));
+    fzk::k4_plan<<<1, 32, 0, (cudaStream_t)stream>>>(G, A, m->S, m->W, (PlanHdr *)p->d_plan);
     ++g_launches;
     fz_status st = cuda_check("k4_plan");
     if (st) {
@@ -764,7 +763,8 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
     a.G = make_gens(m->lay->g, z.d);
     a.n = p->n;
     a.hdr = (PlanHdr *)p->d_plan;
-    a.slices = (const Slice *)(p->d_plan + kPlanHeader);
+    a.Tb = (p->mode == FZ_COUNT) ? m->W : m->S;
+    a.top = z.top;
     a.wt.cardT = m->cardT;
     a.wt.offT = m->offT;
     a.wt.memo = m->rows;

@@ -670,8 +670,14 @@ __global__ void __launch_bounds__(32) k3_chain(const uint64_t *__restrict__ S, c
                 const uint32_t q = lane + 32 * k;
                 if (q < n) {
                     uint32_t *o = rows + (dst + q) * T;
+                    if constexpr (T == 2) {
+                        *reinterpret_cast<uint2 *>(o) = make_uint2(st[k][0], st[k][1]);
+                    } else if constexpr (T == 4) {
+                        *reinterpret_cast<uint4 *>(o) = make_uint4(st[k][0], st[k][1], st[k][2], st[k][3]);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < T; ++j) o[j] = st[k][j];
+                        for (int j = 0; j < T; ++j) o[j] = st[k][j];
+                    }
                 }
             }
         } else {
@@ -717,8 +723,16 @@ __global__ void __launch_bounds__(32) k3_chain(const uint64_t *__restrict__ S, c
         if (more) stage_group(n_ns, n_so, n_ex, b ^ 1);   // buffer b^1 held group g-1 (done)
         const uint32_t *sb = stage + b * kChainStage * T;
         const uint32_t steps = (uint32_t)((nsteps - g * 32) < 32 ? (nsteps - g * 32) : 32);
-        for (uint32_t l = 0; l < steps; ++l)
-            step(sb, __shfl_sync(kFull, c_ns, l), __shfl_sync(kFull, c_ex, l), shfl_u64(c_so, l), shfl_u64(c_dst, l));
+        const uint64_t dst0 = shfl_u64(c_dst, 0);
+        const uint32_t dstoff = (uint32_t)(c_dst - dst0);   // block starts of one group span < 2^32 rows
+        const unsigned has_suffix = __ballot_sync(kFull, c_ns > 0);
+        for (uint32_t l = 0; l < steps; ++l) {
+            const uint64_t dst = dst0 + __shfl_sync(kFull, dstoff, l);
+            if ((has_suffix >> l) & 1u)
+                step(sb, __shfl_sync(kFull, c_ns, l), __shfl_sync(kFull, c_ex, l), shfl_u64(c_so, l), dst);
+            else
+                step(sb, 0u, 0u, 0ull, dst);
+        }
         c_ns = n_ns;
         c_so = n_so;
         c_dst = n_dst;
@@ -891,14 +905,13 @@ __device__ uint64_t row_rank(const uint64_t *__restrict__ S, uint64_t top, const
     return R;
 }
 
-// K4: shard geometry and slice table, entirely on the device (no host round trip).
+// K4: shard geometry, entirely on the device (no host round trip).  One warp.
 // MAT/HASH cut the rows of Z(n) evenly; COUNT cuts the leading-prefix walk evenly.
-__global__ void __launch_bounds__(256) k4_plan(Gens G, PlanArgs A, const uint64_t *__restrict__ S,
-                                                const uint64_t *__restrict__ W, PlanHdr *hdr, Slice *slices)
+// The slices themselves are unranked by the K5 warp that walks them.
+__global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t *__restrict__ S,
+                                               const uint64_t *__restrict__ W, PlanHdr *hdr)
 {
     const int lane = threadIdx.x & 31;
-    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const bool count_mode = (A.mode == FZ_COUNT);
     const uint64_t *Tb = count_mode ? W : S;
     const uint64_t U = __ldg(Tb + A.n);
@@ -907,54 +920,37 @@ __global__ void __launch_bounds__(256) k4_plan(Gens G, PlanArgs A, const uint64_
     uint64_t slice_len = (len + A.max_slices - 1) / A.max_slices;
     if (slice_len < A.floor_len) slice_len = A.floor_len;
     const uint64_t nslices = (len + slice_len - 1) / slice_len;
-    if (gw == 0) {
-        uint64_t rb = ub, re = ue;
-        if (count_mode) {
-            const uint64_t rows_total = __ldg(S + A.n);
-            uint32_t a[kMaxD];
-            for (int j = 0; j < kMaxD; ++j) a[j] = 0;
-            if (ub < U) {
-                unrank(W, A.top, G, A.L, A.n, ub, a);
-                rb = row_rank(S, A.top, G, A.L, A.n, a);
-            } else {
-                rb = rows_total;
-            }
-            if (ue < U) {
-                unrank(W, A.top, G, A.L, A.n, ue, a);
-                re = row_rank(S, A.top, G, A.L, A.n, a);
-            } else {
-                re = rows_total;
-            }
-        }
-        if (lane == 0) {
-            PlanHdr h;
-            h.result[0] = 0;
-            h.result[1] = 0;
-            h.err = 0;
-            h.total_units = U;
-            h.shard_begin = ub;
-            h.shard_len = len;
-            h.slice_len = slice_len;
-            h.nslices = nslices;
-            h.row_begin = rb;
-            h.rows = re - rb;
-            *hdr = h;
-        }
-    }
-    for (uint64_t s = gw; s < nslices; s += nw) {
-        const uint64_t rel = s * slice_len;
-        const uint64_t sl_len = (len - rel) < slice_len ? (len - rel) : slice_len;
+    uint64_t rb = ub, re = ue;
+    if (count_mode) {
+        const uint64_t rows_total = __ldg(S + A.n);
         uint32_t a[kMaxD];
         for (int j = 0; j < kMaxD; ++j) a[j] = 0;
-        const uint64_t k0 = unrank(Tb, A.top, G, A.L, A.n, ub + rel, a);
-        if (lane == 0) {
-            Slice sl;
-            sl.begin = rel;
-            sl.len = sl_len;
-            sl.k0 = count_mode ? 0 : k0;
-            for (int j = 0; j < kMaxD; ++j) sl.a[j] = a[j];
-            slices[s] = sl;
+        if (ub < U) {
+            unrank(W, A.top, G, A.L, A.n, ub, a);
+            rb = row_rank(S, A.top, G, A.L, A.n, a);
+        } else {
+            rb = rows_total;
         }
+        if (ue < U) {
+            unrank(W, A.top, G, A.L, A.n, ue, a);
+            re = row_rank(S, A.top, G, A.L, A.n, a);
+        } else {
+            re = rows_total;
+        }
+    }
+    if (lane == 0) {
+        PlanHdr h;
+        h.result[0] = 0;
+        h.result[1] = 0;
+        h.err = 0;
+        h.total_units = U;
+        h.shard_begin = ub;
+        h.shard_len = len;
+        h.slice_len = slice_len;
+        h.nslices = nslices;
+        h.row_begin = rb;
+        h.rows = re - rb;
+        *hdr = h;
     }
 }
 
@@ -1032,7 +1028,7 @@ struct WalkTables {
 
 template <int D, int T, int MODE>
 __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
-                                                         const Slice *__restrict__ slices, WalkTables wt,
+                                                         const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base)
 {
     constexpr int L = D - T;
@@ -1043,7 +1039,8 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, Pl
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t n = (uint32_t)n64;
     const uint32_t m = G.g[L - 1];
-    const uint64_t nslices = hdr->nslices;
+    const uint64_t nslices = hdr->nslices, slice_len = hdr->slice_len, shard_begin = hdr->shard_begin,
+                   shard_len = hdr->shard_len;
     if (MODE == FZ_MATERIALIZE && hdr->rows > out_cap_rows) {
         if (threadIdx.x == 0 && blockIdx.x == 0) hdr->err = 1;
         return;
@@ -1056,7 +1053,17 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, Pl
     BlockInfo *bi = binfo[wib];
 
     for (uint64_t s = gw; s < nslices; s += nw) {
-        const Slice sl = slices[s];
+        // K4 slice: units [rel, rel + len) of the shard; unrank its first unit (rows: S, prefixes: W)
+        Slice sl;
+        sl.begin = s * slice_len;
+        sl.len = (shard_len - sl.begin) < slice_len ? (shard_len - sl.begin) : slice_len;
+        {
+            uint32_t ua[kMaxD];
+            const uint64_t k0 = unrank(Tb, top, G, L, n64, shard_begin + sl.begin, ua);
+            sl.k0 = (MODE == FZ_COUNT) ? 0 : k0;
+#pragma unroll
+            for (int j = 0; j < L; ++j) sl.a[j] = ua[j];
+        }
         uint32_t a[L];
 #pragma unroll
         for (int j = 0; j < L; ++j) a[j] = sl.a[j];

@@ -67,8 +67,8 @@ def test_validation_errors(lib):
 def test_workspace_sizes_scale(lib):
     st, b1 = _ws(lib, (11, 13, 17, 19), 2, 30233)
     assert st == 0
-    # memo rows 1 416 553 x 2 x 4 B + u32 ring links 4 B/row + tables (S, W, off, cardT, offT)
+    # memo rows 1 416 553 x 2 x 4 B (dimension-pass fill needs no links) + tables (S, W, off, cardT, offT)
     tables = 8 * 5 * 30233 + 8 * 3 * 30233 + 8 * 30234 + 12 * (30233 + 13)
-    assert 1_416_553 * 12 + tables < b1 < 1_416_553 * 12 + tables + 100_000
+    assert 1_416_553 * 8 + tables < b1 < 1_416_553 * 8 + tables + 100_000
     st, b0 = _ws(lib, (11, 13, 17, 19), 2, 30233, entries=0)
     assert st == 0 and b0 < b1
