@@ -604,23 +604,32 @@ __global__ void __launch_bounds__(32) k3_chain(const uint64_t *__restrict__ S, c
         for (int j = 0; j < T; ++j) st[k][j] = 0;
     uint32_t n = 0;                                      // rows of block i of Z(x)
 
-    // metadata of step s = 32 g + lane: suffix length / start of Z(x), block start of Z(x + h)
-    auto meta = [&](uint64_t g, uint32_t &ns, uint64_t &so, uint64_t &dst) {
+    // metadata of step s = 32 g + lane, raw table values (no arithmetic on the loads, so issuing
+    // them does not stall): ns = S_{i+1}[x] (suffix length), o1 = off[x+1], on = off[xn+1], sn = S_i[xn]
+    struct Raw { uint64_t ns, o1, on, sn; };
+    auto meta_load = [&](uint64_t g, Raw &m) {
         const uint64_t s = g * 32 + lane;
-        ns = 0; so = 0; dst = 0;
+        m.ns = 0; m.o1 = 0; m.on = 0; m.sn = 0;
         if (s < nsteps) {
             const uint64_t x = r + s * h, xn = x + h;
-            ns = (uint32_t)__ldg(Si1 + x);
-            so = __ldg(off + x + 1) - ns;
-            dst = __ldg(off + xn + 1) - __ldg(Si + xn);
+            m.ns = __ldg(Si1 + x);
+            m.o1 = __ldg(off + x + 1);
+            m.on = __ldg(off + xn + 1);
+            m.sn = __ldg(Si + xn);
         }
+    };
+    // suffix rows of Z(x) start at o1 - ns; block i of Z(xn) starts at on - sn
+    auto meta = [&](const Raw &m, uint32_t &ns, uint64_t &so, uint64_t &dst) {
+        ns = (uint32_t)m.ns;
+        so = m.o1 - m.ns;
+        dst = m.on - m.sn;
     };
     // stage the suffix rows of group g into buffer b (excl = row position of this lane's step)
     auto stage_group = [&](uint32_t ns, uint64_t so, uint32_t excl, int b) {
         uint32_t *sb = stage + b * kChainStage * T;
-        for (int l = 0; l < 32; ++l) {
+        for (unsigned msk = __ballot_sync(kFull, ns > 0); msk; msk &= msk - 1) {
+            const int l = __ffs(msk) - 1;
             const uint32_t nl = __shfl_sync(kFull, ns, l);
-            if (nl == 0) continue;
             const uint32_t el = __shfl_sync(kFull, excl, l);
             const uint64_t sl = shfl_u64(so, l);
             for (uint32_t j = lane; j < nl && el + j < (uint32_t)kChainStage; j += 32)
@@ -705,19 +714,26 @@ __global__ void __launch_bounds__(32) k3_chain(const uint64_t *__restrict__ S, c
             __syncwarp();
         }
     };
+    // software pipeline over 32-step groups: metadata loaded two groups ahead, suffix rows staged one
+    // group ahead (cp.async), so no group waits on a global load
     uint32_t c_ns, n_ns = 0, n_ex = 0;
     uint64_t c_so, c_dst, n_so = 0, n_dst = 0;
-    meta(0, c_ns, c_so, c_dst);
+    Raw fr;
+    const uint64_t ngroups = (nsteps + 31) / 32;
+    {
+        Raw r0, r1;
+        meta_load(0, r0);
+        meta_load(1, r1);
+        meta(r0, c_ns, c_so, c_dst);
+        meta(r1, n_ns, n_so, n_dst);
+    }
     uint32_t c_ex = scan(c_ns);
     stage_group(c_ns, c_so, c_ex, 0);
-    const uint64_t ngroups = (nsteps + 31) / 32;
     for (uint64_t g = 0; g < ngroups; ++g) {
         const int b = (int)(g & 1);
         const bool more = g + 1 < ngroups;
-        if (more) {
-            meta(g + 1, n_ns, n_so, n_dst);
-            n_ex = scan(n_ns);
-        }
+        meta_load(g + 2, fr);   // consumed at group g+1 (zeros past the end)
+        if (more) n_ex = scan(n_ns);
         cp_async_wait_all();   // group g is staged
         __syncwarp();
         if (more) stage_group(n_ns, n_so, n_ex, b ^ 1);   // buffer b^1 held group g-1 (done)
@@ -726,17 +742,57 @@ __global__ void __launch_bounds__(32) k3_chain(const uint64_t *__restrict__ S, c
         const uint64_t dst0 = shfl_u64(c_dst, 0);
         const uint32_t dstoff = (uint32_t)(c_dst - dst0);   // block starts of one group span < 2^32 rows
         const unsigned has_suffix = __ballot_sync(kFull, c_ns > 0);
-        for (uint32_t l = 0; l < steps; ++l) {
-            const uint64_t dst = dst0 + __shfl_sync(kFull, dstoff, l);
-            if ((has_suffix >> l) & 1u)
-                step(sb, __shfl_sync(kFull, c_ns, l), __shfl_sync(kFull, c_ex, l), shfl_u64(c_so, l), dst);
-            else
-                step(sb, 0u, 0u, 0ull, dst);
+        uint32_t l = 0;
+        while (l < steps) {
+            const unsigned rest = (l < 32) ? (has_suffix & (0xffffffffu << l)) : 0u;
+            const uint32_t lend = rest ? min((uint32_t)(__ffs(rest) - 1), steps) : steps;
+            if constexpr (K > 0) {
+                // steps without suffix rows: the block only gets +1 in coordinate i per step, so four
+                // steps are stored from the current state (+1, +2, +3, +4) with their shuffles batched
+                for (; l + 4 <= lend; l += 4) {
+                    uint32_t d[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) d[u] = __shfl_sync(kFull, dstoff, l + u);
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const uint32_t q = lane + 32 * k;
+                        if (q < n) {
+                            uint32_t *ob = rows + (dst0 + q) * T;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                uint32_t v[T];
+#pragma unroll
+                                for (int j = 0; j < T; ++j) v[j] = st[k][j] + (u + 1) * inc[j];
+                                uint32_t *o = ob + (uint64_t)d[u] * T;
+                                if constexpr (T == 2) {
+                                    *reinterpret_cast<uint2 *>(o) = make_uint2(v[0], v[1]);
+                                } else if constexpr (T == 4) {
+                                    *reinterpret_cast<uint4 *>(o) = make_uint4(v[0], v[1], v[2], v[3]);
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < T; ++j) o[j] = v[j];
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+#pragma unroll
+                        for (int j = 0; j < T; ++j) st[k][j] += 4 * inc[j];
+                }
+            }
+            for (; l < lend; ++l) step(sb, 0u, 0u, 0ull, dst0 + __shfl_sync(kFull, dstoff, l));
+            if (l < steps) {
+                step(sb, __shfl_sync(kFull, c_ns, l), __shfl_sync(kFull, c_ex, l), shfl_u64(c_so, l),
+                     dst0 + __shfl_sync(kFull, dstoff, l));
+                ++l;
+            }
         }
         c_ns = n_ns;
         c_so = n_so;
         c_dst = n_dst;
         c_ex = n_ex;
+        meta(fr, n_ns, n_so, n_dst);
         __syncwarp();
     }
 }
