@@ -171,10 +171,10 @@ def run_native(args, rank, world, local_rank):
     launches = fz.launch_count() - launches0
     ms_total = e0.elapsed_time(e1)
     k5_ms = sum(a.elapsed_time(b) for a, b in k5_events) / args.steps
-    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    tt = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_total = float(tt.item())
     # r_step is the all-reduced {rows} accumulator for N > 1: every rank's rows of the step
     rows_per_step = float(r_step)
     value = rows_per_step * args.steps / (ms_total / 1e3)
