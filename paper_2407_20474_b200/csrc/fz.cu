@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -109,7 +110,7 @@ fz_status host_tables(const uint32_t *g, int d, int L, uint64_t top, HostTables 
 }
 
 struct Layout {
-    uint64_t S, W, cardT, off, offT, chunk, links, rows, counter, total;
+    uint64_t S, W, cardT, off, offT, chunk, links, rows, counter, list, total;
 };
 
 struct Sizing {
@@ -122,6 +123,8 @@ struct Sizing {
     uint32_t Q = 1;             // fill mode 1: batches the bulk stores may lag behind
     uint64_t max_batch_rows = 0;
     uint64_t level_block[FZ_MAX_D] = {0};   // fill mode 4: largest block i of any Z(x), per tail level
+    uint64_t list_cap = 0;                   // fill mode 5: rows per chain list (max_x S_{L+i}[x] over levels)
+    uint64_t list_bytes = 0;
     uint64_t smem_bytes = 0;    // fill mode 1: dynamic shared memory
     int fill_mode = 0;
     Layout lay{};
@@ -228,19 +231,23 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
             uint64_t mb = 0;
             for (uint64_t x = 0; x < top; ++x) mb = std::max<uint64_t>(mb, Si[x] - Si1[x]);
             z.level_block[i] = mb;
-            if (mb > 128 && 2ull * 256 * 4 * t + mb * 4ull * t > kSmemMax) chains_fit = false;
+            if (3ull * 512 * 4 * t + mb * 4ull * t + 6 * 1024 + 16 > kSmemMax) chains_fit = false;
         }
+        // mode 5: one lazy list per residue chain and level, list_cap rows each
+        uint64_t chains_max = 0;
+        for (int i = 0; i + 1 < t; ++i) {
+            const uint64_t *Si = H.S.data() + (size_t)(L + i) * top;
+            uint64_t mx = 0;
+            for (uint64_t x = 0; x < top; ++x) mx = std::max<uint64_t>(mx, Si[x]);
+            z.list_cap = std::max<uint64_t>(z.list_cap, mx);
+            chains_max = std::max<uint64_t>(chains_max, std::min<uint64_t>(g[L + i], top));
+        }
+        z.list_bytes = chains_max * z.list_cap * 4ull * t;
         const int forced = g_fill_override;
-        if (forced >= 1 && forced <= 4 && !(forced == 1 && !fit) && !(forced == 4 && !chains_fit))
+        if (forced >= 1 && forced <= 5 && !(forced == 1 && !fit) && !(forced == 4 && !chains_fit))
             z.fill_mode = forced;
-        else if (entries >= (1ull << 25) || entries / z.batches > 16384)
-            z.fill_mode = 3;
-        else if (chains_fit)
-            z.fill_mode = 4;
-        else if (fit && entries < (1ull << 31) && ring < (1ull << 27))
-            z.fill_mode = 1;
         else
-            z.fill_mode = 2;
+            z.fill_mode = 5;
     } else {
         z.fill_mode = 0;
     }
@@ -257,7 +264,8 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
     l.links = p;
     if (z.fill_mode == 1) p = align_up(p + 4ull * entries + 64, 256);
     if (z.fill_mode == 2) p = align_up(p + 8ull * entries, 256);
-    l.rows = p;    p = align_up(p + rows_bytes, 256);
+    l.rows = p;    p = align_up(p + rows_bytes + 64, 256);
+    l.list = p;    if (z.fill_mode == 5) p = align_up(p + z.list_bytes, 256);
     l.total = p;
     return FZ_OK;
 }
@@ -305,12 +313,13 @@ constexpr uint64_t kPlanHeader = 256;
 
 uint64_t max_slices()
 {
-    return (uint64_t)device_sms() * 8 * (fzk::kWalkThreads / 32) * 4;
+    static const char *e = getenv("FZ_SLICES_PER_WARP");
+    const uint64_t per_warp = (e && atoi(e) > 0) ? (uint64_t)atoi(e) : 16;
+    return (uint64_t)device_sms() * 4 * (fzk::kWalkThreads / 32) * per_warp;
 }
 
 uint64_t plan_bytes() { return kPlanHeader; }   // the header; slices are unranked inside K5
 
-unsigned walk_blocks() { return (unsigned)device_sms() * 8; }
 
 template <int T>
 fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
@@ -327,6 +336,23 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
         ++g_launches;
         return cuda_check("k3_fill_ring");
     }
+    if (z.fill_mode == 5) {
+        const uint32_t h_last = m->lay->g[z.d - 1];
+        const unsigned blocks = (unsigned)std::min<uint64_t>((z.top + 255) / 256, (uint64_t)device_sms() * 8);
+        fzk::k3_last_level<T><<<std::max(blocks, 1u), 256, 0, s>>>(m->S, m->off, m->rows, z.top, z.L, h_last);
+        ++g_launches;
+        fz_status st = cuda_check("k3_last_level");
+        const unsigned wblocks = (unsigned)std::min<uint64_t>((z.top * 32 + 255) / 256, (uint64_t)device_sms() * 16);
+        uint32_t *list = (uint32_t *)(m->ws + z.lay.list);
+        for (int i = T - 2; i >= 0 && !st; --i) {
+            const uint32_t h = m->lay->g[z.L + i];
+            fzk::k3_scan_a<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.L, i, h);
+            fzk::k3_scan_b<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.L, i, h);
+            g_launches += 2;
+            st = cuda_check("k3_scan");
+        }
+        return st;
+    }
     if (z.fill_mode == 4) {
         const uint32_t h_last = m->lay->g[z.d - 1];
         const unsigned blocks = (unsigned)std::min<uint64_t>((z.top + 255) / 256, (uint64_t)device_sms() * 8);
@@ -335,18 +361,16 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
         fz_status st = cuda_check("k3_last_level");
         for (int i = T - 2; i >= 0 && !st; --i) {
             const uint32_t h = m->lay->g[z.L + i];
-            const uint64_t mb = z.level_block[i];
+            const uint64_t cap = std::max<uint64_t>(z.level_block[i], 1);
             const unsigned chains = (unsigned)std::min<uint64_t>(h, z.top);
-            const size_t stage = 2ull * fzk::kChainStage * T * 4;
-            if (mb <= 32) fzk::k3_chain<T, 1><<<chains, 32, stage, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
-            else if (mb <= 64) fzk::k3_chain<T, 2><<<chains, 32, stage, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
-            else if (mb <= 96) fzk::k3_chain<T, 3><<<chains, 32, stage, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
-            else if (mb <= 128) fzk::k3_chain<T, 4><<<chains, 32, stage, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
-            else {
-                const size_t smem = stage + mb * 4ull * T;
-                FZ_CUDA(cudaFuncSetAttribute(fzk::k3_chain<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                fzk::k3_chain<T, 0><<<chains, 32, smem, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h);
-            }
+            // warps per chain: enough to fill the GPU, at most 16
+            static const char *pe = getenv("FZ_CHAIN_P");
+            const unsigned pmax = (pe && atoi(pe) > 1) ? (unsigned)atoi(pe) : 8;
+            const unsigned P = (unsigned)std::max<uint64_t>(2, std::min<uint64_t>(pmax, (uint64_t)device_sms() * 8 / chains));
+            const size_t smem = (((cap * T + 3) & ~3ull) + (size_t)fzk::kStageSlots * fzk::kChainStage * T) * 4 +
+                                (size_t)fzk::kMetaSlots * 4 * 32 * 8 + 2 * 32 * 8 + 2 * 32 * 4;
+            FZ_CUDA(cudaFuncSetAttribute(fzk::k3_chain<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            fzk::k3_chain<T><<<chains, 32 * P, smem, s>>>(m->S, m->off, m->rows, z.top, z.L, i, h, (uint32_t)cap);
             ++g_launches;
             st = cuda_check("k3_chain");
         }
@@ -405,8 +429,17 @@ struct WalkArgs {
 template <int D, int T, int MODE>
 fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
 {
-    fzk::k5_walk<D, T, MODE><<<walk_blocks(), fzk::kWalkThreads, 0, s>>>(a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out,
-                                                                         a.cap, a.row_base);
+    // persistent grid: exactly the resident CTAs (the walk is a grid-stride loop over slices)
+    static thread_local int per_sm = 0;
+    if (!per_sm) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::kWalkThreads, 0) !=
+                cudaSuccess ||
+            per_sm < 1)
+            per_sm = 4;
+        per_sm = std::min(per_sm, 8);
+    }
+    fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::kWalkThreads, 0, s>>>(
+        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base);
     ++g_launches;
     return cuda_check("k5_walk");
 }
@@ -518,7 +551,7 @@ extern "C" {
 const char *fz_last_error(void) { return g_err.c_str(); }
 uint64_t fz_launch_count(void) { return g_launches; }
 void fz_set_memo_cap(uint64_t bytes) { g_memo_cap = bytes ? bytes : 8000000000ull; }
-void fz_set_fill_mode(int mode) { g_fill_override = (mode >= 1 && mode <= 4) ? mode : 0; }
+void fz_set_fill_mode(int mode) { g_fill_override = (mode >= 1 && mode <= 5) ? mode : 0; }
 
 fz_status fz_layout_create(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out)
 {

@@ -59,6 +59,7 @@ struct PlanHdr {
     uint64_t nslices;
     uint64_t row_begin;    // global row index of the shard's first row
     uint64_t rows;         // rows of Z(n) in this shard
+    unsigned long long next_slice;   // K5 work queue (slices are claimed with atomicAdd)
 };
 static_assert(sizeof(PlanHdr) <= 256, "plan header");
 
@@ -577,223 +578,231 @@ __device__ __forceinline__ void cp_async4(void *dst, const void *src)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-constexpr int kChainStage = 256;   // staged suffix rows per 32-step group
+constexpr int kChainStage = 512;   // staged suffix rows per 32-position group
+constexpr int kMetaSlots = 6;      // metadata ring (groups g-1 .. g+4 live)
+constexpr int kStageSlots = 3;     // suffix staging ring (groups g .. g+2 live)
 
-// K > 0: block rows in registers, row q at lane q % 32, slot q / 32 (block <= 32 K rows).
-// K = 0: block rows in dynamic shared memory (cap rows).
-template <int T, int K>
-__global__ void __launch_bounds__(32) k3_chain(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
-                                                uint32_t *rows, uint64_t top, int L, int i, uint32_t h)
+__device__ __forceinline__ void cp_async8(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// One CTA per residue chain r of tail level i (h = h_i), P = blockDim/32 warps.
+// Chain position j: x_j = r + j h.  block_i(Z(x_{j+1})) = incr_i(block_i(Z(x_j)) ++ suffix(x_j)),
+// suffix(x) = Z_{>=i+1}(x) (rows from earlier passes).  Unrolled, block_i(Z(x_{j+1})) is every
+// suffix row appended at positions j' <= j, incremented (j + 1 - j') times, in append order.  The
+// state is therefore an append-only list: a row appended at position j' is kept as row - j' e_i
+// and read back as + (j + 1) e_i.  Warp 0 appends each 32-position group; after one CTA barrier
+// every warp stores the blocks of its share of the group's positions (j = w mod P).  Warp 0 keeps
+// a cp.async pipeline: per-position table values four groups ahead (shared ring), suffix rows two
+// groups ahead (shared staging ring), so no step waits on global memory.
+// Shared memory: buf[cap*T] | stage[3][kChainStage*T] | meta[6][4][32] u64 | desc dst[2][32] u64, rows[2][32] u32.
+// Needs P >= 2 (warp 0 produces, warps 1.. store).
+template <int T>
+__global__ void __launch_bounds__(512) k3_chain(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                                 uint32_t *rows, uint64_t top, int L, int i, uint32_t h, uint32_t cap)
 {
     extern __shared__ __align__(16) uint32_t csh[];
-    uint32_t *stage = csh;                               // [2][kChainStage * T]
-    uint32_t *blk = csh + 2 * kChainStage * T;          // K == 0: block rows
-    const int lane = threadIdx.x;
+    uint32_t *buf = csh;
+    uint32_t *stage = csh + (((uint64_t)cap * T + 3) & ~3ull);
+    uint64_t *meta = reinterpret_cast<uint64_t *>(stage + kStageSlots * kChainStage * T);   // [slot][field][lane]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, P = blockDim.x >> 5;
     const uint64_t r = blockIdx.x;
     if (r + h >= top) return;
     const uint64_t *Si = S + (uint64_t)(L + i) * top;
     const uint64_t *Si1 = S + (uint64_t)(L + i + 1) * top;
-    const uint64_t nsteps = (top - 1 - r) / h;          // x = r + s h, s < nsteps, has x + h < top
+    const uint64_t npos = (top - 1 - r) / h;            // positions j < npos have x_{j+1} < top
+    const uint64_t ngroups = (npos + 31) / 32;
     uint32_t inc[T];
 #pragma unroll
     for (int j = 0; j < T; ++j) inc[j] = (j == i) ? 1u : 0u;
-    uint32_t st[K > 0 ? K : 1][T];
-#pragma unroll
-    for (int k = 0; k < (K > 0 ? K : 1); ++k)
-#pragma unroll
-        for (int j = 0; j < T; ++j) st[k][j] = 0;
-    uint32_t n = 0;                                      // rows of block i of Z(x)
-
-    // metadata of step s = 32 g + lane, raw table values (no arithmetic on the loads, so issuing
-    // them does not stall): ns = S_{i+1}[x] (suffix length), o1 = off[x+1], on = off[xn+1], sn = S_i[xn]
-    struct Raw { uint64_t ns, o1, on, sn; };
-    auto meta_load = [&](uint64_t g, Raw &m) {
-        const uint64_t s = g * 32 + lane;
-        m.ns = 0; m.o1 = 0; m.on = 0; m.sn = 0;
-        if (s < nsteps) {
-            const uint64_t x = r + s * h, xn = x + h;
-            m.ns = __ldg(Si1 + x);
-            m.o1 = __ldg(off + x + 1);
-            m.on = __ldg(off + xn + 1);
-            m.sn = __ldg(Si + xn);
+    // field 0: ns = S_{i+1}[x]; 1: o1 = off[x+1]; 2: on = off[xn+1]; 3: sn = S_i[xn]
+    auto M = [&](uint64_t g, int f) -> uint64_t * { return meta + ((g % kMetaSlots) * 4 + f) * 32; };
+    auto meta_issue = [&](uint64_t g) {   // warp 0
+        const uint64_t j = g * 32 + lane;
+        if (j < npos) {
+            const uint64_t x = r + j * h, xn = x + h;
+            cp_async8(M(g, 0) + lane, Si1 + x);
+            cp_async8(M(g, 1) + lane, off + x + 1);
+            cp_async8(M(g, 2) + lane, off + xn + 1);
+            cp_async8(M(g, 3) + lane, Si + xn);
+        } else {
+            M(g, 0)[lane] = 0;
+            M(g, 1)[lane] = 0;
+            M(g, 2)[lane] = 0;
+            M(g, 3)[lane] = 0;
         }
     };
-    // suffix rows of Z(x) start at o1 - ns; block i of Z(xn) starts at on - sn
-    auto meta = [&](const Raw &m, uint32_t &ns, uint64_t &so, uint64_t &dst) {
-        ns = (uint32_t)m.ns;
-        so = m.o1 - m.ns;
-        dst = m.on - m.sn;
+    auto scan = [&](uint32_t v) {
+        uint32_t s2 = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t u = __shfl_up_sync(kFull, s2, o);
+            if (lane >= o) s2 += u;
+        }
+        return s2 - v;
     };
-    // stage the suffix rows of group g into buffer b (excl = row position of this lane's step)
-    auto stage_group = [&](uint32_t ns, uint64_t so, uint32_t excl, int b) {
-        uint32_t *sb = stage + b * kChainStage * T;
+    auto stage_issue = [&](uint64_t g) {   // warp 0; metadata of group g is complete
+        uint32_t *sb = stage + (g % kStageSlots) * kChainStage * T;
+        const uint32_t ns = (uint32_t)M(g, 0)[lane];
+        const uint64_t so = M(g, 1)[lane] - ns;
+        const uint32_t ex = scan(ns);
         for (unsigned msk = __ballot_sync(kFull, ns > 0); msk; msk &= msk - 1) {
             const int l = __ffs(msk) - 1;
             const uint32_t nl = __shfl_sync(kFull, ns, l);
-            const uint32_t el = __shfl_sync(kFull, excl, l);
+            const uint32_t el = __shfl_sync(kFull, ex, l);
             const uint64_t sl = shfl_u64(so, l);
             for (uint32_t j = lane; j < nl && el + j < (uint32_t)kChainStage; j += 32)
 #pragma unroll
                 for (int w = 0; w < T; ++w) cp_async4(sb + (el + j) * T + w, rows + (sl + j) * T + w);
         }
+    };
+    // store descriptors of a group: block start (u64), rows, increment count, double-buffered
+    uint64_t *ddst = meta + kMetaSlots * 4 * 32;                     // [2][32]
+    uint32_t *dnr = reinterpret_cast<uint32_t *>(ddst + 2 * 32);     // [2][32]
+    if (warp == 0) {   // prologue: metadata of groups 0..3, then suffix rows of groups 0, 1
+        for (uint64_t g = 0; g < 4; ++g) meta_issue(g);
         cp_async_commit();
-    };
-    auto scan = [&](uint32_t v) {
-        uint32_t inc2 = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t u = __shfl_up_sync(kFull, inc2, o);
-            if (lane >= o) inc2 += u;
-        }
-        return inc2 - v;
-    };
-    // one chain step: block of Z(x + h) = incr_i(block of Z(x) ++ suffix rows of Z(x))
-    auto step = [&](const uint32_t *sb, uint32_t ns, uint32_t ex, uint64_t so, uint64_t dst) {
-        auto srow = [&](uint32_t j, int q) -> uint32_t {
-            return (ex + j < (uint32_t)kChainStage) ? sb[(ex + j) * T + q] : rows[(so + j) * T + q];
-        };
-        if constexpr (K > 0) {
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-#pragma unroll
-                for (int j = 0; j < T; ++j) st[k][j] += inc[j];
-            for (uint32_t j0 = 0; j0 < ns; j0 += 32) {
-                const uint32_t base = n + j0;
-                const uint32_t jj = (uint32_t)(lane - (int)base) & 31u;   // suffix row landing on this lane
-                const uint32_t js = j0 + jj;
-                if (js < ns) {
-                    uint32_t w[T];
-#pragma unroll
-                    for (int q = 0; q < T; ++q) w[q] = srow(js, q) + inc[q];
-                    const uint32_t slot = (base + jj) >> 5;
-#pragma unroll
-                    for (int k = 0; k < K; ++k)
-                        if (k == (int)slot)
-#pragma unroll
-                            for (int q = 0; q < T; ++q) st[k][q] = w[q];
-                }
-            }
-            n += ns;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const uint32_t q = lane + 32 * k;
-                if (q < n) {
-                    uint32_t *o = rows + (dst + q) * T;
-                    if constexpr (T == 2) {
-                        *reinterpret_cast<uint2 *>(o) = make_uint2(st[k][0], st[k][1]);
-                    } else if constexpr (T == 4) {
-                        *reinterpret_cast<uint4 *>(o) = make_uint4(st[k][0], st[k][1], st[k][2], st[k][3]);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < T; ++j) o[j] = st[k][j];
-                    }
-                }
-            }
-        } else {
-            for (uint32_t q = lane; q < n; q += 32) {
-                uint32_t *bq = blk + q * T;
-                uint32_t *o = rows + (dst + q) * T;
-#pragma unroll
-                for (int j = 0; j < T; ++j) {
-                    const uint32_t v = bq[j] + inc[j];
-                    bq[j] = v;
-                    o[j] = v;
-                }
-            }
-            for (uint32_t j = lane; j < ns; j += 32) {
-                uint32_t *bq = blk + (n + j) * T;
-                uint32_t *o = rows + (dst + n + j) * T;
-#pragma unroll
-                for (int q = 0; q < T; ++q) {
-                    const uint32_t v = srow(j, q) + inc[q];
-                    bq[q] = v;
-                    o[q] = v;
-                }
-            }
-            n += ns;
-            __syncwarp();
-        }
-    };
-    // software pipeline over 32-step groups: metadata loaded two groups ahead, suffix rows staged one
-    // group ahead (cp.async), so no group waits on a global load
-    uint32_t c_ns, n_ns = 0, n_ex = 0;
-    uint64_t c_so, c_dst, n_so = 0, n_dst = 0;
-    Raw fr;
-    const uint64_t ngroups = (nsteps + 31) / 32;
-    {
-        Raw r0, r1;
-        meta_load(0, r0);
-        meta_load(1, r1);
-        meta(r0, c_ns, c_so, c_dst);
-        meta(r1, n_ns, n_so, n_dst);
-    }
-    uint32_t c_ex = scan(c_ns);
-    stage_group(c_ns, c_so, c_ex, 0);
-    for (uint64_t g = 0; g < ngroups; ++g) {
-        const int b = (int)(g & 1);
-        const bool more = g + 1 < ngroups;
-        meta_load(g + 2, fr);   // consumed at group g+1 (zeros past the end)
-        if (more) n_ex = scan(n_ns);
-        cp_async_wait_all();   // group g is staged
+        cp_async_wait<0>();
         __syncwarp();
-        if (more) stage_group(n_ns, n_so, n_ex, b ^ 1);   // buffer b^1 held group g-1 (done)
-        const uint32_t *sb = stage + b * kChainStage * T;
-        const uint32_t steps = (uint32_t)((nsteps - g * 32) < 32 ? (nsteps - g * 32) : 32);
-        const uint64_t dst0 = shfl_u64(c_dst, 0);
-        const uint32_t dstoff = (uint32_t)(c_dst - dst0);   // block starts of one group span < 2^32 rows
-        const unsigned has_suffix = __ballot_sync(kFull, c_ns > 0);
-        uint32_t l = 0;
-        while (l < steps) {
-            const unsigned rest = (l < 32) ? (has_suffix & (0xffffffffu << l)) : 0u;
-            const uint32_t lend = rest ? min((uint32_t)(__ffs(rest) - 1), steps) : steps;
-            if constexpr (K > 0) {
-                // steps without suffix rows: the block only gets +1 in coordinate i per step, so four
-                // steps are stored from the current state (+1, +2, +3, +4) with their shuffles batched
-                for (; l + 4 <= lend; l += 4) {
-                    uint32_t d[4];
+        stage_issue(0);
+        stage_issue(1);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+    uint32_t nbase = 0;                                  // rows appended before the producer's group
+    // iteration g: warp 0 appends group g and publishes its store descriptors; warps 1..P-1 store
+    // group g-1 (appended one iteration earlier; the list is append-only, so no conflict)
+    for (uint64_t g = 0; g <= ngroups; ++g) {
+        if (warp == 0) {
+            if (g < ngroups) {
+                cp_async_wait<1>();   // everything issued up to iteration g-2: meta(g+2), stage(g)
+                __syncwarp();
+                meta_issue(g + 4);
+                stage_issue(g + 2);
+                cp_async_commit();
+                // append group g: a row appended at position j' is kept as row - j' e_i
+                const uint32_t *sb = stage + (g % kStageSlots) * kChainStage * T;
+                const uint32_t ns = (uint32_t)M(g, 0)[lane];
+                const uint64_t so = M(g, 1)[lane] - ns;
+                const uint32_t ex = scan(ns);
+                for (unsigned msk = __ballot_sync(kFull, ns > 0); msk; msk &= msk - 1) {
+                    const int l = __ffs(msk) - 1;
+                    const uint32_t nl = __shfl_sync(kFull, ns, l);
+                    const uint32_t el = __shfl_sync(kFull, ex, l);
+                    const uint64_t sl = shfl_u64(so, l);
+                    const uint32_t jabs = (uint32_t)(g * 32 + l);
+                    for (uint32_t q = lane; q < nl; q += 32) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) d[u] = __shfl_sync(kFull, dstoff, l + u);
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const uint32_t q = lane + 32 * k;
-                        if (q < n) {
-                            uint32_t *ob = rows + (dst0 + q) * T;
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                uint32_t v[T];
-#pragma unroll
-                                for (int j = 0; j < T; ++j) v[j] = st[k][j] + (u + 1) * inc[j];
-                                uint32_t *o = ob + (uint64_t)d[u] * T;
-                                if constexpr (T == 2) {
-                                    *reinterpret_cast<uint2 *>(o) = make_uint2(v[0], v[1]);
-                                } else if constexpr (T == 4) {
-                                    *reinterpret_cast<uint4 *>(o) = make_uint4(v[0], v[1], v[2], v[3]);
-                                } else {
-#pragma unroll
-                                    for (int j = 0; j < T; ++j) o[j] = v[j];
-                                }
-                            }
+                        for (int w = 0; w < T; ++w) {
+                            const uint32_t v =
+                                (el + q < (uint32_t)kChainStage) ? sb[(el + q) * T + w] : rows[(sl + q) * T + w];
+                            buf[(nbase + el + q) * T + w] = v - jabs * inc[w];
                         }
                     }
+                }
+                // block_i(Z(x_{j+1})) = first nbase + ex + ns rows (+ (j + 1) e_i), stored at on - sn
+                ddst[(g & 1) * 32 + lane] = M(g, 2)[lane] - M(g, 3)[lane];
+                dnr[(g & 1) * 32 + lane] = nbase + ex + ns;
+                nbase += __shfl_sync(kFull, ex + ns, 31);
+            }
+        } else if (g > 0) {
+            const uint64_t gp = g - 1;
+            const uint64_t *dd = ddst + (gp & 1) * 32;
+            const uint32_t *dn = dnr + (gp & 1) * 32;
+            const int Pc = P - 1;
+            const uint32_t first = (uint32_t)((Pc - (int)((gp * 32) % Pc) + (warp - 1)) % Pc);
+            for (uint32_t l = first; l < 32 && gp * 32 + l < npos; l += Pc) {
+                const uint64_t d = dd[l];
+                const uint32_t nr = dn[l];
+                const uint32_t c = (uint32_t)(gp * 32 + l + 1);
+                for (uint32_t q = lane; q < nr; q += 32) {
+                    uint32_t v[T];
 #pragma unroll
-                    for (int k = 0; k < K; ++k)
+                    for (int w = 0; w < T; ++w) v[w] = buf[q * T + w] + c * inc[w];
+                    uint32_t *o = rows + (d + q) * T;
+                    if constexpr (T == 2) {
+                        *reinterpret_cast<uint2 *>(o) = make_uint2(v[0], v[1]);
+                    } else if constexpr (T == 4) {
+                        *reinterpret_cast<uint4 *>(o) = make_uint4(v[0], v[1], v[2], v[3]);
+                    } else {
 #pragma unroll
-                        for (int j = 0; j < T; ++j) st[k][j] += 4 * inc[j];
+                        for (int w = 0; w < T; ++w) o[w] = v[w];
+                    }
                 }
             }
-            for (; l < lend; ++l) step(sb, 0u, 0u, 0ull, dst0 + __shfl_sync(kFull, dstoff, l));
-            if (l < steps) {
-                step(sb, __shfl_sync(kFull, c_ns, l), __shfl_sync(kFull, c_ex, l), shfl_u64(c_so, l),
-                     dst0 + __shfl_sync(kFull, dstoff, l));
-                ++l;
+        }
+        __syncthreads();
+    }
+    if (warp == 0) cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------- K3 scan
+// Fill mode 5 (default): the chain recurrence of mode 4 evaluated in its unrolled form.
+// For chain r of level i (h = h_i), the lazy list of the chain holds, at positions
+// [S_i[x] - S_{i+1}[x], S_i[x]), the suffix Z_{>=i+1}(x) of x = r + j h, each row minus j e_i;
+// its prefix of length S_i[x] is Z_{>=i}(x) (lazy).  Since S_i[x] - S_{i+1}[x] = S_i[x - h]
+// (PAPER.md:163-166 bookkeeping, suffix-table recurrence) the segments tile the list, so
+//   phase A: every x writes its suffix rows into its chain list       (parallel over x)
+//   phase B: block_i(Z(x)) = list prefix of length S_i[x] - S_{i+1}[x], + (x div h) e_i
+//            (= incr_i applied x div h - j' times to the row appended at position j')
+// -- the same copy-and-increment results, with no dependency between x values inside a pass.
+template <int T>
+__global__ void __launch_bounds__(256) k3_scan_a(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                                  const uint32_t *rows, uint32_t *list, uint64_t cap_list, uint64_t top,
+                                                  int L, int i, uint32_t h)
+{
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t *Si = S + (uint64_t)(L + i) * top, *Si1 = Si + top;
+    for (uint64_t x = gw; x + h < top; x += nw) {
+        const uint64_t ns = __ldg(Si1 + x);
+        if (ns == 0) continue;
+        const uint64_t so = __ldg(off + x + 1) - ns, base = __ldg(Si + x) - ns;
+        const uint32_t j = (uint32_t)(x / h), r = (uint32_t)(x - (uint64_t)j * h);
+        uint32_t *lr = list + ((uint64_t)r * cap_list + base) * T;
+        for (uint64_t k = lane; k < ns; k += 32) {
+            const uint32_t *src = rows + (so + k) * T;
+#pragma unroll
+            for (int w = 0; w < T; ++w) lr[k * T + w] = __ldcg(src + w) - (w == i ? j : 0u);
+        }
+    }
+}
+
+template <int T>
+__global__ void __launch_bounds__(256) k3_scan_b(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                                  uint32_t *rows, const uint32_t *list, uint64_t cap_list, uint64_t top,
+                                                  int L, int i, uint32_t h)
+{
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t *Si = S + (uint64_t)(L + i) * top, *Si1 = Si + top;
+    for (uint64_t x = h + gw; x < top; x += nw) {
+        const uint64_t si = __ldg(Si + x);
+        const uint64_t nb = si - __ldg(Si1 + x);
+        if (nb == 0) continue;
+        const uint64_t dst = __ldg(off + x + 1) - si;
+        const uint32_t c = (uint32_t)(x / h), r = (uint32_t)(x - (uint64_t)c * h);
+        const uint32_t *lr = list + (uint64_t)r * cap_list * T;
+        for (uint64_t q = lane; q < nb; q += 32) {
+            uint32_t v[T];
+#pragma unroll
+            for (int w = 0; w < T; ++w) v[w] = __ldcg(lr + q * T + w) + (w == i ? c : 0u);
+            uint32_t *o = rows + (dst + q) * T;
+            if constexpr (T == 2) {
+                *reinterpret_cast<uint2 *>(o) = make_uint2(v[0], v[1]);
+            } else if constexpr (T == 4) {
+                *reinterpret_cast<uint4 *>(o) = make_uint4(v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int w = 0; w < T; ++w) o[w] = v[w];
             }
         }
-        c_ns = n_ns;
-        c_so = n_so;
-        c_dst = n_dst;
-        c_ex = n_ex;
-        meta(fr, n_ns, n_so, n_dst);
-        __syncwarp();
     }
 }
 
@@ -1006,6 +1015,7 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
         h.nslices = nslices;
         h.row_begin = rb;
         h.rows = re - rb;
+        h.next_slice = 0;
         *hdr = h;
     }
 }
@@ -1108,7 +1118,13 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, Pl
     uint64_t acc_rows = 0, acc_hash = 0;
     BlockInfo *bi = binfo[wib];
 
-    for (uint64_t s = gw; s < nslices; s += nw) {
+    (void)gw;
+    (void)nw;
+    for (;;) {
+        uint64_t s = 0;
+        if (lane == 0) s = atomicAdd(&hdr->next_slice, 1ull);
+        s = shfl_u64(s, 0);
+        if (s >= nslices) break;
         // K4 slice: units [rel, rel + len) of the shard; unrank its first unit (rows: S, prefixes: W)
         Slice sl;
         sl.begin = s * slice_len;
@@ -1178,33 +1194,47 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, Pl
                     bi[e].v = (uint32_t)vv;
                 }
                 __syncwarp();
-                // flattened copy: rows q0 + lane of the round, owner block via block-start bitmask
+                // flattened copy: rows q0 + lane of the round, owner block via block-start bitmask.
+                // UNR chunks of 32 rows are resolved and their memo tails loaded before any store,
+                // so each lane keeps UNR L2 loads in flight.
+                constexpr int UNR = (MODE == FZ_MATERIALIZE) ? 4 : 1;
                 int e0 = 0;
-                for (uint32_t q0 = 0; q0 < use; q0 += 32) {
-                    const unsigned bit = (cc > 0 && excl >= q0 && excl - q0 < 32) ? (1u << (excl - q0)) : 0u;
-                    const unsigned M = __reduce_or_sync(kFull, bit);
-                    if (q0 != 0) e0 += (int)(M & 1u);
-                    const uint32_t q = q0 + lane;
-                    if (q < use) {
+                for (uint32_t q0 = 0; q0 < use; q0 += 32 * UNR) {
+                    uint32_t wv[UNR][D];
+                    bool ok[UNR];
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) {
+                        const uint32_t qb = q0 + 32 * u;
+                        const unsigned bit = (cc > 0 && excl >= qb && excl - qb < 32) ? (1u << (excl - qb)) : 0u;
+                        const unsigned M = __reduce_or_sync(kFull, bit);
+                        if (qb != 0) e0 += (int)(M & 1u);
+                        const uint32_t q = qb + lane;
+                        ok[u] = q < use;
                         const int e = e0 + __popc(M & ((2u << lane) - 2u));
-                        const BlockInfo info = bi[e];
-                        uint32_t w[D];
+                        e0 += __popc(M & 0xfffffffeu);
+                        if (ok[u]) {
+                            const BlockInfo info = bi[e];
 #pragma unroll
-                        for (int j = 0; j < L - 1; ++j) w[j] = a[j];
-                        w[L - 1] = info.v;
-                        if constexpr (T > 0) {
-                            uint32_t tw[T];
-                            load_tail<T>(wt.memo + (info.memo_row + (q - info.start)) * T, tw);
+                            for (int j = 0; j < L - 1; ++j) wv[u][j] = a[j];
+                            wv[u][L - 1] = info.v;
+                            if constexpr (T > 0) {
+                                uint32_t tw[T];
+                                load_tail<T>(wt.memo + (info.memo_row + (q - info.start)) * T, tw);
 #pragma unroll
-                            for (int j = 0; j < T; ++j) w[L + j] = tw[j];
-                        }
-                        if constexpr (MODE == FZ_MATERIALIZE) {
-                            store_row<D>(out + (outpos + q) * (uint64_t)D, w);
-                        } else {
-                            acc_hash += row_hash<D>(row_base + outpos + q, w);
+                                for (int j = 0; j < T; ++j) wv[u][L + j] = tw[j];
+                            }
                         }
                     }
-                    e0 += __popc(M & 0xfffffffeu);
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) {
+                        if (!ok[u]) continue;
+                        const uint32_t q = q0 + 32 * u + lane;
+                        if constexpr (MODE == FZ_MATERIALIZE) {
+                            store_row<D>(out + (outpos + q) * (uint64_t)D, wv[u]);
+                        } else {
+                            acc_hash += row_hash<D>(row_base + outpos + q, wv[u]);
+                        }
+                    }
                 }
                 __syncwarp();
                 acc_rows += (lane == 0) ? use : 0;

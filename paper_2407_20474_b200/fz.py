@@ -111,7 +111,7 @@ def set_memo_cap(nbytes: int) -> None:
 
 
 def set_fill_mode(mode: int) -> None:
-    """Force the memo copy-increment schedule (1 ring, 2 L2, 3 grid, 4 chains; 0 = automatic)."""
+    """Force the memo copy-increment schedule (1 ring, 2 L2, 3 grid, 4 chains, 5 chain scan; 0 = automatic)."""
     _L.fz_set_fill_mode(int(mode))
 
 

@@ -49,11 +49,12 @@ MEMO_CASES = [((9, 20), 25), ((9, 20), 1001), ((17, 19), 30233), ((41, 43), 1735
               ((38, 40, 41, 42), 3001), ((3, 5, 8), 500), ((1, 1, 2), 200), ((7,), 300), ((4, 6, 10, 4), 400)]
 
 
-@pytest.mark.parametrize("fill", [0, 1, 2, 3, 4], ids=lambda m: f"fill{m}")
+@pytest.mark.parametrize("fill", [0, 1, 2, 3, 4, 5], ids=lambda m: f"fill{m}")
 @pytest.mark.parametrize("tail,top", MEMO_CASES, ids=lambda x: str(x))
 def test_memo_rows_vs_alg2(tail, top, fill, corc):
     """K1-K3 memo == Alg 2 over the tail generators, row by row, for every
-    copy-increment schedule (0 automatic, 1 ring, 2 L2, 3 grid, 4 dimension passes)."""
+    copy-increment schedule (0 automatic, 1 ring, 2 L2, 3 grid, 4 dimension passes, 5 dimension
+    passes in scan form)."""
     g = (5,) + tuple(tail)          # a leading generator, the memo is over the last t = len(tail)
     t = len(tail)
     fz.set_fill_mode(fill)
