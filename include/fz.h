@@ -143,6 +143,10 @@ fz_status fz_count(const fz_memo *m, uint64_t n, void *stream, uint64_t *count);
 fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards, uint64_t *row_begin,
                         uint64_t *rows);
 
+/* Same cut from a layout alone (host only, no device memory or GPU needed). */
+fz_status fz_layout_shard_rows(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, uint64_t *row_begin,
+                               uint64_t *rows);
+
 /* Device plan-workspace bytes (a fixed bound: 256-B header + 64 B per slice,
  * at most 32 x (resident warps) slices). */
 fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t *bytes);

@@ -711,6 +711,21 @@ fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards,
     return FZ_OK;
 }
 
+fz_status fz_layout_shard_rows(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, uint64_t *row_begin,
+                               uint64_t *rows)
+{
+    if (!lay || nshards < 1) return fail(FZ_EINVAL, "NULL layout or nshards < 1");
+    if (n >= lay->z.top) return fail(FZ_EINVAL, "n >= top");
+    if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode");
+    for (int s = 0; s < nshards; ++s) {
+        uint64_t rb, rl;
+        host_shard(lay, n, mode, nshards, s, rb, rl);
+        if (row_begin) row_begin[s] = rb;
+        if (rows) rows[s] = rl;
+    }
+    return FZ_OK;
+}
+
 fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t *bytes)
 {
     if (!bytes) return fail(FZ_EINVAL, "bytes is NULL");

@@ -53,6 +53,7 @@ def _load():
         "fz_layout_workspace_bytes": [vp, u64p],
         "fz_layout_get_info": [vp, ctypes.POINTER(_MemoInfo)],
         "fz_memo_build_layout": [vp, vp, u64, vp, ctypes.POINTER(vp)],
+        "fz_layout_shard_rows": [vp, u64, c_int, c_int, u64p, u64p],
         "fz_enumerate_launch": [vp, vp, u64, u64, vp],
         "fz_plan_result": [vp, vp, u64p, u64p],
         "fz_plan_result_ptr": [vp, ctypes.POINTER(vp)],
@@ -130,6 +131,13 @@ class Layout:
         info = _MemoInfo()
         _check(_L.fz_layout_get_info(self.h, ctypes.byref(info)))
         self.info = {k: getattr(info, k) for k, _ in _MemoInfo._fields_}
+
+    def shard_rows(self, n: int, mode, nshards: int):
+        """Host-side shard cut (same as the device planner K4): (row_begin list, rows list)."""
+        rb = (ctypes.c_uint64 * nshards)()
+        rl = (ctypes.c_uint64 * nshards)()
+        _check(_L.fz_layout_shard_rows(self.h, int(n), _mode(mode), nshards, rb, rl))
+        return list(rb), list(rl)
 
     def __del__(self):
         h = getattr(self, "h", None)
