@@ -641,7 +641,9 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
         FZ_CUDA(cudaMemsetAsync(m->counter, 0, 256, s));
         unsigned int *counter = m->counter;
         void *args[] = {&G, &tb, &counter};
-        const int blocks = std::min(device_sms(), kMaxGrid);
+        static const char *ge = getenv("FZ_K1_GRID");
+        const int want = (ge && atoi(ge) > 0) ? atoi(ge) : device_sms();
+        const int blocks = std::min(std::min(device_sms(), kMaxGrid), want);
         FZ_CUDA(cudaLaunchCooperativeKernel((const void *)fzk::k1_tables, blocks, 1024, args, 0, s));
         ++g_launches;
         return cuda_check("k1_tables");

@@ -206,18 +206,34 @@ __global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned in
     __shared__ uint64_t sm[40];
     unsigned int target = 0;
     const uint64_t top = tb.top;
-    const int d = tb.d, L = tb.L;
+    const int d = tb.d, L = tb.L, t = d - L;
     const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t x = gt; x < top; x += ng) {
-        tb.S[(uint64_t)d * top + x] = (x == 0) ? 1ull : 0ull;
-        tb.W[(uint64_t)L * top + x] = 1ull;
+    // Phase 0: the base levels and, in closed form, the first scan of each table:
+    //   S_d[x] = [x = 0], S_{d-1}[x] = [g_{d-1} | x];  W_L[x] = 1, W_{L-1}[x] = floor(x / g_{L-1}) + 1.
+    {
+        const uint64_t gd = G.g[d - 1], gl = G.g[L - 1];
+        for (uint64_t x = gt; x < top; x += ng) {
+            tb.S[(uint64_t)d * top + x] = (x == 0) ? 1ull : 0ull;
+            tb.S[(uint64_t)(d - 1) * top + x] = (x % gd == 0) ? 1ull : 0ull;
+            tb.W[(uint64_t)L * top + x] = 1ull;
+            tb.W[(uint64_t)(L - 1) * top + x] = x / gl + 1;
+        }
     }
-    grid_barrier(counter, target);
-    for (int p = 0; p < d; ++p) {
+    // Phases p >= 1: S_{d-1-p} and W_{L-1-p} by column scans (one CTA per residue class), and the
+    // CSR scan of card = S_L as soon as S_L is final (end of phase t-1; phase 0 when t <= 1):
+    // off stage A (per-CTA chunk sums) at phase pa, stage B (chunk scan, off, residue-major copies)
+    // at phase pa + 1.  d - 1 + (extra off phases) grid barriers in total.
+    const int pa = t > 1 ? t : 1;
+    const int nphase = (d > pa + 2) ? d : pa + 2;
+    const uint64_t *card = tb.S + (uint64_t)L * top;
+    const uint64_t CH = (top + gridDim.x - 1) / gridDim.x;
+    const uint64_t c0 = blockIdx.x * CH, c1 = (c0 + CH < top) ? c0 + CH : top;
+    for (int p = 1; p < nphase; ++p) {
+        grid_barrier(counter, target);
         const int i = d - 1 - p, j = L - 1 - p;
-        const uint64_t gi = G.g[i];
-        const uint64_t ncolS = gi < top ? gi : top;
+        const uint64_t gi = i >= 0 ? G.g[i] : 1;
+        const uint64_t ncolS = i >= 0 ? (gi < top ? gi : top) : 0;
         const uint64_t gj = j >= 0 ? G.g[j] : 1;
         const uint64_t ncolW = j >= 0 ? (gj < top ? gj : top) : 0;
         for (uint64_t c = blockIdx.x; c < ncolS + ncolW; c += gridDim.x) {
@@ -226,40 +242,34 @@ __global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned in
             else
                 block_column_scan(tb.W + (uint64_t)(j + 1) * top, tb.W + (uint64_t)j * top, top, gj, c - ncolS, sm);
         }
-        grid_barrier(counter, target);
-    }
-    // K2: off = exclusive scan of card = S_L over [0, top); chunk per CTA.
-    const uint64_t *card = tb.S + (uint64_t)L * top;
-    const uint64_t CH = (top + gridDim.x - 1) / gridDim.x;
-    const uint64_t c0 = blockIdx.x * CH, c1 = (c0 + CH < top) ? c0 + CH : top;
-    {
-        uint64_t s = 0;
-        for (uint64_t x = c0 + threadIdx.x; x < c1; x += blockDim.x) s += __ldcg(card + x);
-        uint64_t tot;
-        block_excl_scan(s, sm, &tot);
-        if (threadIdx.x == 0) tb.chunk[blockIdx.x] = tot;
-    }
-    grid_barrier(counter, target);
-    {
-        uint64_t pre = 0;
-        for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += __ldcg(tb.chunk + b);
-        uint64_t tot;
-        pre = block_excl_scan(pre, sm, &tot);   // reduce: tot = sum of chunk[0..bid)
-        pre = tot;
-        const uint64_t m = tb.m;
-        for (uint64_t xb = c0; xb < c1; xb += blockDim.x) {
-            const uint64_t x = xb + threadIdx.x;
-            const uint64_t v = x < c1 ? __ldcg(card + x) : 0;
-            uint64_t t2;
-            const uint64_t ex = pre + block_excl_scan(v, sm, &t2);
-            if (x < c1) {
-                tb.off[x] = ex;
-                const uint64_t ti = (x % m) * tb.R + x / m;
-                tb.cardT[ti] = (uint32_t)v;
-                tb.offT[ti] = ex;
-                if (x + 1 == top) tb.off[top] = ex + v;
+        if (p == pa) {   // K2 stage A: chunk sums of card
+            uint64_t s = 0;
+            for (uint64_t x = c0 + threadIdx.x; x < c1; x += blockDim.x) s += __ldcg(card + x);
+            uint64_t tot;
+            block_excl_scan(s, sm, &tot);
+            if (threadIdx.x == 0) tb.chunk[blockIdx.x] = tot;
+        }
+        if (p == pa + 1) {   // K2 stage B: off = exclusive scan of card; residue-major cardT / offT
+            uint64_t pre = 0;
+            for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += __ldcg(tb.chunk + b);
+            uint64_t tot;
+            block_excl_scan(pre, sm, &tot);
+            pre = tot;
+            const uint64_t m = tb.m;
+            for (uint64_t xb = c0; xb < c1; xb += blockDim.x) {
+                const uint64_t x = xb + threadIdx.x;
+                const uint64_t v = x < c1 ? __ldcg(card + x) : 0;
+                uint64_t t2;
+                const uint64_t ex = pre + block_excl_scan(v, sm, &t2);
+                if (x < c1) {
+                    tb.off[x] = ex;
+                    const uint64_t ti = (x % m) * tb.R + x / m;
+                    tb.cardT[ti] = (uint32_t)v;
+                    tb.offT[ti] = ex;
+                    if (x + 1 == top) tb.off[top] = ex + v;
+                }
+                pre += t2;
             }
-            pre += t2;
         }
     }
     if (tb.link_mode == 0) return;
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned in
     // links: row q of Z(x; tail) lies in block i (0-based tail index) with start
     // card[x] - S_{L+i}[x] ("beginning index of Z_{>=i}"); it is
     // incr_i of row off[y+1] - S_{L+i}[y] + k of Z(y), y = x - g_{L+i}, k = q - start.
-    const int lane = threadIdx.x & 31, t = tb.t;
+    const int lane = threadIdx.x & 31;
     const uint64_t gw = gt >> 5, nw = ng >> 5;
     if (gw == 0 && lane == 0) {
         if (tb.link_mode == 1) ((uint32_t *)tb.links)[0] = kZeroLink32;
@@ -984,6 +994,7 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
     const uint64_t len = ue - ub;
     uint64_t slice_len = (len + A.max_slices - 1) / A.max_slices;
     if (slice_len < A.floor_len) slice_len = A.floor_len;
+    if (slice_len > (1ull << 31)) slice_len = 1ull << 31;   // K5 COUNT keeps the budget in 32 bits
     const uint64_t nslices = (len + slice_len - 1) / slice_len;
     uint64_t rb = ub, re = ue;
     if (count_mode) {
@@ -1117,6 +1128,7 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, Pl
     const uint64_t *__restrict__ offT = wt.offT;
     uint64_t acc_rows = 0, acc_hash = 0;
     BlockInfo *bi = binfo[wib];
+    const uint32_t cgq = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] / m : 0, cgr = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] % m : 0;
 
     (void)gw;
     (void)nw;
@@ -1148,24 +1160,58 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, Pl
         uint64_t kfirst = sl.k0;
         uint64_t left = sl.len;
         uint64_t outpos = sl.begin;
-        while (left > 0) {
-            if constexpr (MODE == FZ_COUNT) {
-                // the run v, v-1, ..., 0 is the contiguous segment [colbase - v, colbase]
-                const uint64_t run = (uint64_t)v + 1;
-                const uint64_t take = run < left ? run : left;
-                const uint32_t *seg = cardT + (colbase - (uint64_t)v);
-                uint64_t o = 0;
-                for (; o + 128 <= take; o += 128) {
-                    const uint32_t c0 = __ldg(seg + o + lane), c1 = __ldg(seg + o + 32 + lane);
-                    const uint32_t c2 = __ldg(seg + o + 64 + lane), c3 = __ldg(seg + o + 96 + lane);
-                    acc_rows += (uint64_t)c0 + c1 + c2 + c3;
+        if constexpr (MODE == FZ_COUNT) {
+            // COUNT walk: every leading prefix adds card[p], p = n - phi(prefix).  The innermost run
+            // v, v-1, .., 0 is the contiguous residue-major segment [col R + q - v, col R + q]; the
+            // common carry (a_{L-1} > 0) moves r_in by g_{L-1} without a division.
+            uint32_t q = r_in / m, col = r_in - q * m;
+            uint32_t vv = (uint32_t)v;
+            uint32_t left32 = (uint32_t)left;   // K4 keeps COUNT slices below 2^31 prefixes
+            for (;;) {
+                const uint32_t run = vv + 1;
+                const uint32_t take = left32 < run ? left32 : run;
+                const uint32_t *p = cardT + ((uint64_t)col * wt.R + (q - vv) + lane);
+                uint32_t rem = take;
+                for (; rem >= 128; rem -= 128, p += 128)
+                    acc_rows += (uint64_t)(__ldg(p) + __ldg(p + 32)) + (__ldg(p + 64) + __ldg(p + 96));
+                uint32_t part = 0;
+                if ((uint32_t)lane < rem) part += __ldg(p);
+                if ((uint32_t)lane + 32 < rem) part += __ldg(p + 32);
+                if ((uint32_t)lane + 64 < rem) part += __ldg(p + 64);
+                if ((uint32_t)lane + 96 < rem) part += __ldg(p + 96);
+                acc_rows += part;
+                left32 -= take;
+                left = left32;
+                if (left == 0 || L == 1) break;
+                if (a[L - 2] > 0) {
+                    a[L - 2] -= 1;
+                    col += cgr;
+                    if (col >= m) {
+                        col -= m;
+                        ++q;
+                    }
+                    q += cgq;
+                } else {
+                    int i = -1;
+#pragma unroll
+                    for (int j = 0; j < L - 1; ++j)
+                        if (a[j] > 0) i = j;
+                    if (i < 0) break;   // end of stream
+                    uint32_t r = n;
+#pragma unroll
+                    for (int j = 0; j < L - 1; ++j) {
+                        if (j == i) a[j] -= 1;
+                        if (j > i) a[j] = r / G.g[j];
+                        r -= a[j] * G.g[j];
+                    }
+                    q = r / m;
+                    col = r - q * m;
                 }
-                for (; o < take; o += 32)
-                    if (o + lane < take) acc_rows += __ldg(seg + o + lane);
-                left -= take;
-                if (left == 0) break;
-                v = -1;
-            } else {
+                vv = q;
+            }
+        } else {
+        while (left > 0) {
+            {
                 const int32_t vv = v - lane;
                 const bool valid = vv >= 0;
                 const uint64_t ti = colbase - (uint64_t)v + lane;
@@ -1269,6 +1315,7 @@ __global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, Pl
             const uint32_t q = r_in / m;
             v = (int32_t)q;
             colbase = (uint64_t)(r_in - q * m) * wt.R + q;
+        }
         }
     }
     acc_rows = warp_sum_u64(acc_rows);
