@@ -1052,18 +1052,20 @@ __device__ __forceinline__ uint64_t row_hash(uint64_t k, const uint32_t (&w)[D])
     return x;
 }
 
+// Memo-row loads and output stores as volatile PTX: they keep program order, so a warp issues the
+// loads of all its UNR chunks before the first store (UNR L2 loads in flight per lane).
 template <int T>
 __device__ __forceinline__ void load_tail(const uint32_t *__restrict__ p, uint32_t *w)
 {
     if constexpr (T == 2) {
-        uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
-        w[0] = v.x; w[1] = v.y;
+        asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "l"(p));
     } else if constexpr (T == 4) {
-        uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
-        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                     : "l"(p));
     } else {
 #pragma unroll
-        for (int j = 0; j < T; ++j) w[j] = __ldg(p + j);
+        for (int j = 0; j < T; ++j) asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(w[j]) : "l"(p + j));
     }
 }
 
@@ -1072,19 +1074,17 @@ __device__ __forceinline__ void store_row(uint32_t *p, const uint32_t (&w)[D])
 {
     if constexpr (D % 4 == 0) {
 #pragma unroll
-        for (int j = 0; j < D; j += 4) {
-            uint4 v = make_uint4(w[j], w[j + 1], w[j + 2], w[j + 3]);
-            __stcs(reinterpret_cast<uint4 *>(p + j), v);
-        }
+        for (int j = 0; j < D; j += 4)
+            asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p + j), "r"(w[j]), "r"(w[j + 1]),
+                         "r"(w[j + 2]), "r"(w[j + 3])
+                         : "memory");
     } else if constexpr (D % 2 == 0) {
 #pragma unroll
-        for (int j = 0; j < D; j += 2) {
-            uint2 v = make_uint2(w[j], w[j + 1]);
-            __stcs(reinterpret_cast<uint2 *>(p + j), v);
-        }
+        for (int j = 0; j < D; j += 2)
+            asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p + j), "r"(w[j]), "r"(w[j + 1]) : "memory");
     } else {
 #pragma unroll
-        for (int j = 0; j < D; ++j) __stcs(p + j, w[j]);
+        for (int j = 0; j < D; ++j) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + j), "r"(w[j]) : "memory");
     }
 }
 
@@ -1104,7 +1104,7 @@ struct WalkTables {
 };
 
 template <int D, int T, int MODE>
-__global__ void __launch_bounds__(kWalkThreads) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
+__global__ void __launch_bounds__(kWalkThreads, 2) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base)
 {
