@@ -59,7 +59,7 @@ typedef struct fz_memo fz_memo; /* opaque host handle; references the caller's w
 
 typedef struct {
     int d;                  /* dimension */
-    int t;                  /* memo dimension (tail generators tabulated), 0 <= t <= d-1 */
+    int t;                  /* memo dimension (tail generators tabulated), 0 <= t <= d */
     uint64_t top;           /* memo covers every x in [0, top) */
     uint64_t entries;       /* total memo rows = sum_{x<top} |Z(x; tail)| */
     uint64_t max_card;      /* max_x |Z(x; tail)| */
@@ -76,7 +76,9 @@ typedef struct {
 /* Validate (gens, d, t, top) and return the device workspace bytes
  * fz_memo_build needs.  with_entries = 0 sizes the count tables only (enough
  * for FZ_COUNT and fz_count).  t = 0 means no memo (plain bounded walk, the
- * prior-work nextCandidate); d = 1 requires t = 0.
+ * prior-work nextCandidate); t = d builds the full DP table
+ * (Alg 2/3's product F[m] for every m < top),
+ * in which Z(n) is the block Memo[n].
  * Errors: FZ_EINVAL (d, t, gens, top = 0), FZ_ERANGE (a table entry >= 2^64,
  * top > 2^32), FZ_ECAP (memo rows * t * 4 B above the cap). */
 fz_status fz_memo_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t top, int with_entries,
@@ -98,6 +100,12 @@ typedef struct fz_layout fz_layout;
 fz_status fz_layout_create(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out);
 fz_status fz_layout_workspace_bytes(const fz_layout *lay, uint64_t *bytes);
 void fz_layout_free(fz_layout *lay);
+
+/* Memo-dimension recommendation (PAPER.md:301 observes that the best memoDim
+ * depends on the instance): predicted seconds per t in 0..d written to cost[0..d] (optional,
+ * +inf-like 1e300 when infeasible: t = 0 or d, or a memo above the cap), best t in *t_best.
+ * Host only (count tables of gens up to n); model constants in fz.cu. */
+fz_status fz_recommend_t(const uint32_t *gens, int d, uint64_t n, fz_mode mode, int *t_best, double *cost);
 
 /* ------------------------------------------------------------- A2-A4 -- */
 /* Build the memo on the GPU (asynchronous on `stream`):

@@ -137,7 +137,7 @@ fz_status validate(const uint32_t *g, int d, int t, uint64_t top)
 {
     if (!g) return fail(FZ_EINVAL, "gens is NULL");
     if (d < 1 || d > FZ_MAX_D) return fail(FZ_EINVAL, "d=%d outside [1, %d]", d, FZ_MAX_D);
-    if (t < 0 || t > d - 1) return fail(FZ_EINVAL, "t=%d outside [0, d-1=%d]", t, d - 1);
+    if (t < 0 || t > d) return fail(FZ_EINVAL, "t=%d outside [0, d=%d]", t, d);
     for (int i = 0; i < d; ++i)
         if (g[i] == 0) return fail(FZ_EINVAL, "g_%d = 0 (generators must be positive)", i + 1);
     if (top == 0) return fail(FZ_EINVAL, "top must be >= 1");
@@ -251,7 +251,7 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
     } else {
         z.fill_mode = 0;
     }
-    const uint64_t m = g[L - 1];
+    const uint64_t m = L > 0 ? g[L - 1] : 1;
     Layout &l = z.lay;
     uint64_t p = 256;                                   // header
     l.S = p;       p = align_up(p + 8ull * (d + 1) * top, 256);
@@ -472,6 +472,25 @@ fz_status launch_walk(int d, int t, int mode, const WalkArgs &a, cudaStream_t s)
     }
 }
 
+template <int D = 1>
+fz_status launch_table(int d, int mode, const WalkArgs &a, const uint64_t *off, cudaStream_t s)
+{
+    if constexpr (D <= FZ_MAX_D) {
+        if (d != D) return launch_table<D + 1>(d, mode, a, off, s);
+        const unsigned blocks = (unsigned)device_sms() * 4;
+        if (mode == FZ_MATERIALIZE)
+            fzk::k5_table<D, FZ_MATERIALIZE><<<blocks, 256, 0, s>>>(a.hdr, off, a.n, a.wt.memo, a.out, a.cap, a.row_base);
+        else if (mode == FZ_COUNT)
+            fzk::k5_table<D, FZ_COUNT><<<blocks, 256, 0, s>>>(a.hdr, off, a.n, a.wt.memo, a.out, a.cap, a.row_base);
+        else
+            fzk::k5_table<D, FZ_HASH><<<blocks, 256, 0, s>>>(a.hdr, off, a.n, a.wt.memo, a.out, a.cap, a.row_base);
+        ++g_launches;
+        return cuda_check("k5_table");
+    } else {
+        return fail(FZ_EINVAL, "d=%d not instantiated", d);
+    }
+}
+
 // host-side rank / unrank over the layout's host tables (fz_shard_rows, fz_run_host)
 uint64_t host_row_rank(const fz_layout *lay, uint64_t n, const uint32_t *a)
 {
@@ -509,7 +528,7 @@ uint64_t mul_div_h(uint64_t U, uint64_t a, uint64_t b) { return (U / b) * a + ((
 void host_shard(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, int s, uint64_t &rb, uint64_t &rl)
 {
     const uint64_t rows_total = lay->H.S[n];
-    if (mode == FZ_COUNT) {
+    if (mode == FZ_COUNT && lay->z.L > 0) {
         const uint64_t P = lay->H.W[n];
         auto rowat = [&](uint64_t pidx) -> uint64_t {
             if (pidx >= P) return rows_total;
@@ -630,7 +649,7 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
     tb.chunk = m->chunk;
     tb.links = m->links;
     tb.top = z.top;
-    tb.m = lay->g[z.L - 1];
+    tb.m = z.L > 0 ? lay->g[z.L - 1] : 1;
     tb.R = (z.top + tb.m - 1) / tb.m;
     tb.d = z.d;
     tb.L = z.L;
@@ -713,6 +732,59 @@ fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards,
     return FZ_OK;
 }
 
+// SURVEY §8(f) f4 (the best memo dimension depends on the instance).  Predicted
+// seconds for memo dimension t, from the host count tables:
+//   rows R = |Z(n)|, leading prefixes P(t), innermost runs Q(t) (leading prefixes without the last
+//   coordinate), memo rows E(t) = sum_{x<=n} |Z(x; tail_t)|;
+//   MATERIALIZE: R 4d / 6.5e12 + 8e-12 P + E 4t / 2e12 + 6e-5
+//   HASH:        4e-12 R + 7.4e-12 P + E 4t / 2e12 + 6e-5
+//   COUNT:       6.2e-11 Q + 1e-13 P + 6e-5        (no memo rows are built)
+// constants: B200 measurements of round 1 (C2, C3 t=2/3, C4 t=3).  Memos above the
+// memory cap are infeasible (cost +inf).
+fz_status fz_recommend_t(const uint32_t *gens, int d, uint64_t n, fz_mode mode, int *t_best, double *cost)
+{
+    if (!t_best) return fail(FZ_EINVAL, "t_best is NULL");
+    fz_status st = validate(gens, d, d > 1 ? 1 : 0, n + 1);
+    if (st) return st;
+    const uint64_t top = n + 1;
+    HostTables H;
+    if ((st = host_tables(gens, d, 0, top, H))) return st;   // S levels (suffix counts) only
+    double best = 1e300;
+    int bt = d > 1 ? 1 : 0;
+    for (int t = 0; t <= d; ++t) {
+        double c = 1e300;
+        const int L = d - t;
+        if (t >= 1 && t <= d - 1) {
+            // P(t): prefixes (a_1..a_L) with phi <= n = sum_{y<=n} |Z(y; g_1..g_L)|; Q(t) with L-1 gens
+            auto cum = [&](int nl) -> double {
+                std::vector<double> c2(top, 0.0);
+                c2[0] = 1;
+                for (int i = 0; i < nl; ++i)
+                    for (uint64_t x = gens[i]; x < top; ++x) c2[x] += c2[x - gens[i]];
+                double sum = 0;
+                for (uint64_t x = 0; x < top; ++x) sum += c2[x];
+                return sum;
+            };
+            const double P = cum(L), Q = cum(L - 1);
+            const double R = (double)H.S[n];
+            double E = 0;
+            const uint64_t *card = H.S.data() + (size_t)L * top;
+            for (uint64_t x = 0; x < top; ++x) E += (double)card[x];
+            const bool fits = E * 4.0 * t <= (double)g_memo_cap;
+            if (mode == FZ_MATERIALIZE && fits) c = R * 4.0 * d / 6.5e12 + 8e-12 * P + E * 4.0 * t / 2e12 + 6e-5;
+            if (mode == FZ_HASH && fits) c = 4e-12 * R + 7.4e-12 * P + E * 4.0 * t / 2e12 + 6e-5;
+            if (mode == FZ_COUNT) c = 6.2e-11 * Q + 1e-13 * P + 6e-5;
+        }
+        if (cost) cost[t] = c;
+        if (c < best) {
+            best = c;
+            bt = t;
+        }
+    }
+    *t_best = bt;
+    return FZ_OK;
+}
+
 fz_status fz_layout_shard_rows(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, uint64_t *row_begin,
                                uint64_t *rows)
 {
@@ -766,7 +838,7 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
     A.n = n;
     A.top = z.top;
     A.max_slices = max_slices();
-    A.floor_len = (mode == FZ_COUNT) ? 1024 : 256;
+    A.floor_len = (mode == FZ_COUNT) ? 1024 : 32;
     A.mode = (int)mode;
     A.shard = shard;
     A.nshards = nshards;
@@ -818,10 +890,12 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
     a.wt.cardT = m->cardT;
     a.wt.offT = m->offT;
     a.wt.memo = m->rows;
-    a.wt.R = (z.top + m->lay->g[z.L - 1] - 1) / m->lay->g[z.L - 1];
+    const uint64_t gl = z.L > 0 ? m->lay->g[z.L - 1] : 1;
+    a.wt.R = (z.top + gl - 1) / gl;
     a.out = d_out;
     a.cap = (p->mode == FZ_MATERIALIZE) ? out_capacity_rows : ~0ull;
     a.row_base = row_base;
+    if (z.L == 0) return launch_table(z.d, (int)p->mode, a, m->off, (cudaStream_t)stream);
     return launch_walk(z.d, z.t, (int)p->mode, a, (cudaStream_t)stream);
 }
 

@@ -212,12 +212,12 @@ __global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned in
     // Phase 0: the base levels and, in closed form, the first scan of each table:
     //   S_d[x] = [x = 0], S_{d-1}[x] = [g_{d-1} | x];  W_L[x] = 1, W_{L-1}[x] = floor(x / g_{L-1}) + 1.
     {
-        const uint64_t gd = G.g[d - 1], gl = G.g[L - 1];
+        const uint64_t gd = G.g[d - 1], gl = L > 0 ? G.g[L - 1] : 1;
         for (uint64_t x = gt; x < top; x += ng) {
             tb.S[(uint64_t)d * top + x] = (x == 0) ? 1ull : 0ull;
             tb.S[(uint64_t)(d - 1) * top + x] = (x % gd == 0) ? 1ull : 0ull;
             tb.W[(uint64_t)L * top + x] = 1ull;
-            tb.W[(uint64_t)(L - 1) * top + x] = x / gl + 1;
+            if (L > 0) tb.W[(uint64_t)(L - 1) * top + x] = x / gl + 1;
         }
     }
     // Phases p >= 1: S_{d-1-p} and W_{L-1-p} by column scans (one CTA per residue class), and the
@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
                                                const uint64_t *__restrict__ W, PlanHdr *hdr)
 {
     const int lane = threadIdx.x & 31;
-    const bool count_mode = (A.mode == FZ_COUNT);
+    const bool count_mode = (A.mode == FZ_COUNT) && A.L > 0;   // t = d (L = 0): rows in every mode
     const uint64_t *Tb = count_mode ? W : S;
     const uint64_t U = __ldg(Tb + A.n);
     const uint64_t ub = mul_div(U, A.shard, A.nshards), ue = mul_div(U, A.shard + 1, A.nshards);
@@ -1323,6 +1323,35 @@ __global__ void __launch_bounds__(kWalkThreads, 2) k5_walk(Gens G, uint64_t n64,
     if constexpr (MODE == FZ_HASH) {
         acc_hash = warp_sum_u64(acc_hash);
         if (lane == 0) atomicAdd((unsigned long long *)(result + 1), (unsigned long long)acc_hash);
+    }
+}
+
+// ------------------------------------------------------------ K5, t = d
+// Full DP table (t = d; Alg 2/3's product): Z(n) is the memo
+// block Memo[n] itself; the shard's rows are copied (MATERIALIZE), counted, or hashed.
+template <int D, int MODE>
+__global__ void __launch_bounds__(256) k5_table(PlanHdr *hdr, const uint64_t *__restrict__ off, uint64_t n,
+                                                 const uint32_t *__restrict__ memo, uint32_t *out, uint64_t out_cap_rows,
+                                                 uint64_t row_base)
+{
+    const uint64_t rows = hdr->rows, rb = hdr->row_begin;
+    if (MODE == FZ_MATERIALIZE && rows > out_cap_rows) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) hdr->err = 1;
+        return;
+    }
+    if (row_base == ~0ull) row_base = rb;
+    const uint64_t base = __ldg(off + n) + rb;
+    uint64_t acc_h = 0;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t w[D];
+        load_tail<D>(memo + (base + r) * D, w);
+        if constexpr (MODE == FZ_MATERIALIZE) store_row<D>(out + r * D, w);
+        if constexpr (MODE == FZ_HASH) acc_h += row_hash<D>(row_base + r, w);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)rows);
+    if constexpr (MODE == FZ_HASH) {
+        acc_h = warp_sum_u64(acc_h);
+        if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long *)(hdr->result + 1), (unsigned long long)acc_h);
     }
 }
 

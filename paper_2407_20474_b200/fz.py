@@ -54,6 +54,7 @@ def _load():
         "fz_layout_get_info": [vp, ctypes.POINTER(_MemoInfo)],
         "fz_memo_build_layout": [vp, vp, u64, vp, ctypes.POINTER(vp)],
         "fz_layout_shard_rows": [vp, u64, c_int, c_int, u64p, u64p],
+        "fz_recommend_t": [u32p, c_int, u64, c_int, ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_double)],
         "fz_enumerate_launch": [vp, vp, u64, u64, vp],
         "fz_plan_result": [vp, vp, u64p, u64p],
         "fz_plan_result_ptr": [vp, ctypes.POINTER(vp)],
@@ -109,6 +110,16 @@ def launch_count() -> int:
 
 def set_memo_cap(nbytes: int) -> None:
     _L.fz_set_memo_cap(nbytes)
+
+
+def recommend_t(gens, n: int, mode="materialize"):
+    """Memo dimension with the lowest predicted time (host cost model, fz_recommend_t).
+    Returns (t, {t: predicted seconds})."""
+    d = len(gens)
+    tb = ctypes.c_int()
+    cost = (ctypes.c_double * (d + 1))()
+    _check(_L.fz_recommend_t(_gens(gens), d, int(n), _mode(mode), ctypes.byref(tb), cost))
+    return tb.value, {t: cost[t] for t in range(d + 1) if cost[t] < 1e299}
 
 
 def set_fill_mode(mode: int) -> None:

@@ -48,7 +48,8 @@ def _ws(lib, gens, t, top, entries=1):
 def test_validation_errors(lib):
     lib.fz_last_error.restype = ctypes.c_char_p
     assert _ws(lib, (6, 9, 20), 2, 1001)[0] == 0
-    assert _ws(lib, (6, 9, 20), 3, 1001)[0] == 1          # t > d-1
+    assert _ws(lib, (6, 9, 20), 3, 1001)[0] == 0          # t = d: full DP table (f1)
+    assert _ws(lib, (6, 9, 20), 4, 1001)[0] == 1          # t > d
     assert _ws(lib, (6, 9, 20), -1, 1001)[0] == 1
     assert _ws(lib, (6, 0, 20), 1, 1001)[0] == 1          # g_i = 0
     assert _ws(lib, (6, 9, 20), 1, 0)[0] == 1             # top = 0
@@ -72,3 +73,16 @@ def test_workspace_sizes_scale(lib):
     assert 1_416_553 * 8 + tables < b1 < 1_416_553 * 8 + tables + 100_000
     st, b0 = _ws(lib, (11, 13, 17, 19), 2, 30233, entries=0)
     assert st == 0 and b0 < b1
+
+
+def test_recommend_t():
+    """f4: the cost model picks the memo dimensions that measured fastest in round 1 and rules out
+    memos above the cap (C2 t=3 is 13 GB, C3 t=4 is 30 GB)."""
+    from paper_2407_20474_b200 import fz
+
+    t, cost = fz.recommend_t((11, 13, 17, 19), 30232, "materialize")
+    assert t == 2 and 3 not in cost and cost[2] < cost[1]
+    t, cost = fz.recommend_t((23, 29, 31, 37, 41, 43), 17350, "hash")
+    assert t == 3 and 4 not in cost and cost[3] < cost[2]
+    t, cost = fz.recommend_t((97, 98, 99, 100, 101, 102, 103, 104), 10000, "count")
+    assert cost[3] < cost[2] < cost[1]

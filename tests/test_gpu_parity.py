@@ -232,3 +232,42 @@ def test_run_host_end_to_end(corc):
         assert np.array_equal(host.numpy().view(np.uint32), want)
         assert fz.run_host(g, t, n, "hash") == (cnt, h)
         assert fz.run_host(g, t, n, "count")[0] == cnt
+
+
+# ------------------------------------------------------- f1: full DP table (t = d)
+def test_full_table_c1(corc):
+    """t = d builds Alg 2/3's whole table F[m], m <= 1000; every
+    Z(m) is then a table block.  Second GPU route for C1; table == Alg 2 row by row."""
+    g, N = C1_GENS, C1_MAX_N
+    memo = fz.memo_build(g, len(g), N + 1)
+    rows, off, _ = memo.views()
+    want_rows, want_off = corc.memo_alg2(g, N + 1)
+    assert np.array_equal(off.cpu().numpy().astype(np.uint64), want_off)
+    assert np.array_equal(_np(rows).reshape(-1, 3), want_rows)
+    tot, hs = 0, 0
+    for m in (0, 1, 43, 44, 500, 999, 1000):
+        out, r, _ = fz.enumerate(memo, m, "materialize")
+        want, cnt, h = corc.enumerate(m, g)
+        assert r == cnt and np.array_equal(_np(out).reshape(-1, 3)[:r], want.reshape(-1, 3))
+        assert fz.enumerate(memo, m, "hash")[1:] == (cnt, h)
+        assert fz.enumerate(memo, m, "count")[1] == cnt
+    for m in range(N + 1):
+        _, r, h = fz.enumerate(memo, m, "hash")
+        tot += r
+        hs = (hs + h) % (1 << 64)
+    assert tot == 162781 and hs == 0x54C291A6F228CA38
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_full_table_random(seed, corc):
+    g, n, _ = random_instance(seed)
+    memo = fz.memo_build(g, len(g), n + 1)
+    want, cnt, h = corc.enumerate(n, g)
+    for ns in (1, 3):
+        parts, hs = [], 0
+        for s in range(ns):
+            out, r, _ = fz.enumerate(memo, n, "materialize", shard=s, nshards=ns)
+            parts.append(_np(out).reshape(-1, len(g))[:r])
+            hs = (hs + fz.enumerate(memo, n, "hash", shard=s, nshards=ns)[2]) % (1 << 64)
+        got = np.concatenate(parts)
+        assert np.array_equal(got, want.reshape(-1, len(g))) and hs == h
