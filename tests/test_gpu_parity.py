@@ -167,10 +167,16 @@ def test_c2_full_materialize(corc):
 
 
 # ---------------------------------------------------------------------- C3
-@pytest.mark.parametrize("t", (2, 3))
+@pytest.mark.parametrize("t", (2, 3, 4))
 def test_c3_count_hash(t, corc):
-    """C3 count+hash: count == GF count, hash == SURVEY App. A KAT, identical for every t."""
-    memo = fz.memo_build(C3_GENS, t, C3_N + 1)
+    """C3 count+hash: count == GF count, hash == SURVEY App. A KAT, identical for every t
+    (t = 4: a 30.4 GB memo of 1.9e9 rows, above the default 8e9 B cap)."""
+    if t == 4:
+        fz.set_memo_cap(64 << 30)
+    try:
+        memo = fz.memo_build(C3_GENS, t, C3_N + 1)
+    finally:
+        fz.set_memo_cap(0)
     _, rows, h = fz.enumerate(memo, C3_N, "hash")
     assert rows == corc.gf_count(C3_N, C3_GENS) == 10_002_178_949
     assert h == 0xBE3AEBC0385B7792

@@ -14,6 +14,9 @@ CFG = {
     "C2c": ((11, 13, 17, 19), 30232, 2, "count"),
     "C3t2": ((23, 29, 31, 37, 41, 43), 17350, 2, "hash"),
     "C3t3": ((23, 29, 31, 37, 41, 43), 17350, 3, "hash"),
+    "C3t4": ((23, 29, 31, 37, 41, 43), 17350, 4, "hash"),
+    "C4t2": ((97, 98, 99, 100, 101, 102, 103, 104), 40000, 2, "count"),
+    "C4t4": ((97, 98, 99, 100, 101, 102, 103, 104), 40000, 4, "count"),
     "C4": ((97, 98, 99, 100, 101, 102, 103, 104), 40000, 3, "count"),
     "T1": ((13, 37, 38, 40, 41, 42, 43, 44), 2000, 4, "materialize"),
 }
@@ -26,6 +29,7 @@ def ev():
 
 
 def main():
+    fz.set_memo_cap(64 << 30)   # C3 t=4: 30.4 GB memo (above the 8e9 default)
     names = sys.argv[1:] or ["C2"]
     for name in names:
         g, n, t, mode = CFG[name]
