@@ -227,6 +227,40 @@ def run_native(args, rank, world, local_rank):
     return res, (g, n, t, mode)
 
 
+def count_mode_extra(local_rank):
+    """Count mode (the metric's second half) on this GPU: C2's element and C4 (t=3), whole step
+    (count tables + plan + the COUNT walk over every leading prefix), CUDA-event timed."""
+    import torch
+
+    from fzinputs import C2, C4
+    from paper_2407_20474_b200 import fz
+
+    res = {}
+    for name, g, n, t, steps in (("C2", C2.gens, C2.n, C2.t, 50), ("C4", C4.gens, C4.n, C4.t, 5)):
+        lay = fz.Layout(g, t, n + 1, entries=False)
+        ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device="cuda")
+        pws = torch.empty(256, dtype=torch.uint8, device="cuda")
+
+        def step():
+            m = fz.Memo(layout=lay, workspace=ws)
+            p = fz.Plan(m, n, "count", workspace=pws)
+            p.launch()
+            return m, p
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        keep = [step() for _ in range(steps)]
+        e1.record()
+        torch.cuda.synchronize()
+        rows, _ = keep[-1][1].result()
+        ms = e0.elapsed_time(e1) / steps
+        res[name] = {"value": rows / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "rows": rows, "t": t,
+                     "workload": f"Z({n}; {','.join(map(str, g))}) count, t={t}"}
+    return res
+
+
 def run_e2e(args, spec, local_rank):
     """Same metric through the C-ABI whole-path call with HOST buffers (fz_run_host)."""
     import torch
@@ -326,6 +360,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C2", "C4"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-count", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = _env_int("WORLD_SIZE", 1)
@@ -355,6 +390,8 @@ def main():
             res["e2e"] = e2e
         if world == 1 and not args.no_cpu:
             res["cpu_baseline"] = cpu_baseline(spec)
+        if world == 1 and args.config == "C2" and not args.no_count:
+            res["count_mode"] = count_mode_extra(local_rank)
         print(json.dumps(res), flush=True)
     if world > 1:
         dist.barrier()
