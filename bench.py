@@ -376,10 +376,16 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # one process per GPU; FZ_BENCH_BACKEND=gloo lets several ranks share one GPU (CI / single-GPU checks)
+    local_rank = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("FZ_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     res, spec = run_native(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_e2e:

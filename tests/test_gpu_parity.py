@@ -277,3 +277,16 @@ def test_full_table_random(seed, corc):
             hs = (hs + fz.enumerate(memo, n, "hash", shard=s, nshards=ns)[2]) % (1 << 64)
         got = np.concatenate(parts)
         assert np.array_equal(got, want.reshape(-1, len(g))) and hs == h
+
+
+@pytest.mark.parametrize("mode", ["materialize", "count", "hash"])
+def test_device_plan_matches_host_cut(mode):
+    """K4 cuts shards on the device; fz_layout_shard_rows makes the same cut on the host."""
+    g, n, t = (13, 37, 38, 40, 41), 3000, 2
+    lay = fz.Layout(g, t, n + 1)
+    memo = fz.Memo(layout=lay)
+    for ns in (1, 2, 5, 8):
+        rb, rl = lay.shard_rows(n, mode, ns)
+        for s in range(ns):
+            p = fz.Plan(memo, n, mode, s, ns)
+            assert (p.row_begin, p.rows) == (rb[s], rl[s]), (mode, ns, s)
