@@ -28,6 +28,7 @@ thread_local std::string g_err;
 thread_local uint64_t g_launches = 0;
 uint64_t g_memo_cap = 8000000000ull;
 int g_fill_override = 0;               // 0 = automatic fill-mode choice
+bool g_fuse_memo = true;               // fill mode 5 inside K1's cooperative launch (FZ_FUSE_MEMO=0 to split)
 
 fz_status fail(fz_status st, const char *fmt, ...)
 {
@@ -403,10 +404,21 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
 }
 
 template <int T = 1>
+const void *memo_kernel(int t)
+{
+    if constexpr (T <= FZ_MAX_D) {
+        if (t == T) return (const void *)fzk::k1_memo<T>;
+        return memo_kernel<T + 1>(t);
+    } else {
+        return nullptr;
+    }
+}
+
+template <int T = 1>
 fz_status launch_fill(const fz_memo *m, cudaStream_t s)
 {
     if (m->lay->z.fill_mode == 0) return FZ_OK;
-    if constexpr (T < FZ_MAX_D) {
+    if constexpr (T <= FZ_MAX_D) {
         if (m->lay->z.t == T) return launch_fill_t<T>(m, s);
         return launch_fill<T + 1>(m, s);
     } else {
@@ -617,6 +629,11 @@ fz_status fz_memo_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t t
 
 fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_bytes, void *stream, fz_memo **out)
 {
+    static const bool fuse_env = [] {
+        const char *e = getenv("FZ_FUSE_MEMO");
+        return !(e && e[0] == '0');
+    }();
+    g_fuse_memo = fuse_env;
     if (!out || !lay) return fail(FZ_EINVAL, "NULL argument");
     *out = nullptr;
     if (!d_ws || ((uintptr_t)d_ws & 255)) return fail(FZ_EINVAL, "workspace NULL or not 256-byte aligned");
@@ -663,11 +680,21 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
         static const char *ge = getenv("FZ_K1_GRID");
         const int want = (ge && atoi(ge) > 0) ? atoi(ge) : device_sms();
         const int blocks = std::min(std::min(device_sms(), kMaxGrid), want);
+        if (z.fill_mode == 5 && g_fuse_memo) {   // count pass + CSR + default fill in one launch
+            uint32_t *rows = m->rows, *list = (uint32_t *)(m->ws + z.lay.list);
+            uint64_t cap_list = z.list_cap;
+            void *args5[] = {&G, &tb, &counter, &rows, &list, &cap_list};
+            const void *fn = memo_kernel(z.t);
+            if (!fn) return fail(FZ_EINVAL, "t=%d not instantiated", z.t);
+            FZ_CUDA(cudaLaunchCooperativeKernel(fn, blocks, 1024, args5, 0, s));
+            ++g_launches;
+            return cuda_check("k1_memo");
+        }
         FZ_CUDA(cudaLaunchCooperativeKernel((const void *)fzk::k1_tables, blocks, 1024, args, 0, s));
         ++g_launches;
         return cuda_check("k1_tables");
     }();
-    if (!st) st = launch_fill(m, s);
+    if (!st && !(z.fill_mode == 5 && g_fuse_memo)) st = launch_fill(m, s);
     if (st) {
         delete m;
         return st;

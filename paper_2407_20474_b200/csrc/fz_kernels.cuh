@@ -201,10 +201,9 @@ __device__ void block_column_scan(const uint64_t *src, uint64_t *dst, uint64_t N
 //   phase p = 0..d-1: S_{d-1-p} = column scan of S_{d-p} mod g_{d-1-p}, and W_{L-1-p} likewise;
 //   card = S_L, off = exclusive scan of card (two phases), residue-major cardT/offT;
 //   links: per memo row, the source row of the copy-increment (see k3_fill_*).
-__global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned int *counter)
+__device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigned int *counter, unsigned int &target,
+                                        uint64_t *sm)
 {
-    __shared__ uint64_t sm[40];
-    unsigned int target = 0;
     const uint64_t top = tb.top;
     const int d = tb.d, L = tb.L, t = d - L;
     const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -272,8 +271,19 @@ __global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned in
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned int *counter)
+{
+    __shared__ uint64_t sm[40];
+    unsigned int target = 0;
+    k1_body(G, tb, counter, target, sm);
     if (tb.link_mode == 0) return;
     grid_barrier(counter, target);
+    const uint64_t top = tb.top;
+    const int L = tb.L, t = tb.t;
+    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
     // links: row q of Z(x; tail) lies in block i (0-based tail index) with start
     // card[x] - S_{L+i}[x] ("beginning index of Z_{>=i}"); it is
     // incr_i of row off[y+1] - S_{L+i}[y] + k of Z(y), y = x - g_{L+i}, k = q - start.
@@ -567,6 +577,22 @@ __global__ void __launch_bounds__(1024) k3_fill_ring(const uint64_t *__restrict_
 
 // last tail dimension: block t-1 of Z(x) = [(0,..,0, x/h)] if h | x (x = 0 gives Memo[0] = [0])
 template <int T>
+__device__ __forceinline__ void last_level_body(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                                uint32_t *rows, uint64_t top, int L, uint32_t h, uint64_t gt,
+                                                uint64_t ng)
+{
+    const uint64_t *Sl = S + (uint64_t)(L + T - 1) * top;
+    for (uint64_t x = gt; x < top; x += ng) {
+        if (x % h) continue;
+        const uint64_t dst = __ldcg(off + x + 1) - __ldcg(Sl + x);
+        uint32_t *o = rows + dst * T;
+#pragma unroll
+        for (int j = 0; j < T - 1; ++j) o[j] = 0;
+        o[T - 1] = (uint32_t)(x / h);
+    }
+}
+
+template <int T>
 __global__ void __launch_bounds__(256) k3_last_level(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                                       uint32_t *rows, uint64_t top, int L, uint32_t h)
 {
@@ -761,13 +787,11 @@ __global__ void __launch_bounds__(512) k3_chain(const uint64_t *__restrict__ S, 
 //            (= incr_i applied x div h - j' times to the row appended at position j')
 // -- the same copy-and-increment results, with no dependency between x values inside a pass.
 template <int T>
-__global__ void __launch_bounds__(256) k3_scan_a(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
-                                                  const uint32_t *rows, uint32_t *list, uint64_t cap_list, uint64_t top,
-                                                  int L, int i, uint32_t h)
+__device__ __forceinline__ void scan_a_body(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                            const uint32_t *rows, uint32_t *list, uint64_t cap_list, uint64_t top,
+                                            int L, int i, uint32_t h, uint64_t gw, uint64_t nw)
 {
     const int lane = threadIdx.x & 31;
-    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t *Si = S + (uint64_t)(L + i) * top, *Si1 = Si + top;
     for (uint64_t x = gw; x + h < top; x += nw) {
         const uint64_t ns = __ldg(Si1 + x);
@@ -784,13 +808,11 @@ __global__ void __launch_bounds__(256) k3_scan_a(const uint64_t *__restrict__ S,
 }
 
 template <int T>
-__global__ void __launch_bounds__(256) k3_scan_b(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
-                                                  uint32_t *rows, const uint32_t *list, uint64_t cap_list, uint64_t top,
-                                                  int L, int i, uint32_t h)
+__device__ __forceinline__ void scan_b_body(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                            uint32_t *rows, const uint32_t *list, uint64_t cap_list, uint64_t top,
+                                            int L, int i, uint32_t h, uint64_t gw, uint64_t nw)
 {
     const int lane = threadIdx.x & 31;
-    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t *Si = S + (uint64_t)(L + i) * top, *Si1 = Si + top;
     for (uint64_t x = h + gw; x < top; x += nw) {
         const uint64_t si = __ldg(Si + x);
@@ -813,6 +835,47 @@ __global__ void __launch_bounds__(256) k3_scan_b(const uint64_t *__restrict__ S,
                 for (int w = 0; w < T; ++w) o[w] = v[w];
             }
         }
+    }
+}
+
+template <int T>
+__global__ void __launch_bounds__(256) k3_scan_a(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                                  const uint32_t *rows, uint32_t *list, uint64_t cap_list, uint64_t top,
+                                                  int L, int i, uint32_t h)
+{
+    scan_a_body<T>(S, off, rows, list, cap_list, top, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
+                   ((uint64_t)gridDim.x * blockDim.x) >> 5);
+}
+
+template <int T>
+__global__ void __launch_bounds__(256) k3_scan_b(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
+                                                  uint32_t *rows, const uint32_t *list, uint64_t cap_list, uint64_t top,
+                                                  int L, int i, uint32_t h)
+{
+    scan_b_body<T>(S, off, rows, list, cap_list, top, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
+                   ((uint64_t)gridDim.x * blockDim.x) >> 5);
+}
+
+// The whole default memo build in ONE cooperative launch: K1 (count pass + CSR) then the fill-mode-5
+// passes of K3 (last level, then per level: chain lists, blocks), separated by grid barriers instead
+// of kernel boundaries.
+template <int T>
+__global__ void __launch_bounds__(1024) k1_memo(Gens G, Tables tb, unsigned int *counter, uint32_t *rows,
+                                                 uint32_t *list, uint64_t cap_list)
+{
+    __shared__ uint64_t sm[40];
+    unsigned int target = 0;
+    k1_body(G, tb, counter, target, sm);
+    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
+    grid_barrier(counter, target);
+    last_level_body<T>(tb.S, tb.off, rows, tb.top, tb.L, G.g[tb.d - 1], gt, ng);
+    for (int i = T - 2; i >= 0; --i) {
+        const uint32_t h = G.g[tb.L + i];
+        grid_barrier(counter, target);
+        scan_a_body<T>(tb.S, tb.off, rows, list, cap_list, tb.top, tb.L, i, h, gt >> 5, ng >> 5);
+        grid_barrier(counter, target);
+        scan_b_body<T>(tb.S, tb.off, rows, list, cap_list, tb.top, tb.L, i, h, gt >> 5, ng >> 5);
     }
 }
 
