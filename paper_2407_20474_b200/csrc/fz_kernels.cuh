@@ -1167,7 +1167,7 @@ struct WalkTables {
 };
 
 template <int D, int T, int MODE>
-__global__ void __launch_bounds__(kWalkThreads, 2) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
+__global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base)
 {
