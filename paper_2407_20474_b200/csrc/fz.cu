@@ -444,14 +444,18 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     // persistent grid: exactly the resident CTAs (the walk is a grid-stride loop over slices)
     static thread_local int per_sm = 0;
     if (!per_sm) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::kWalkThreads, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::kWalkThreads,
+                                                          4096 * 8) !=
                 cudaSuccess ||
             per_sm < 1)
             per_sm = 4;
         per_sm = std::min(per_sm, 8);
     }
-    fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::kWalkThreads, 0, s>>>(
-        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base);
+    // level-0 unrank column in shared memory when it is short (<= 4096 entries, 32 KB)
+    const uint64_t f0 = a.n / a.G.g[0] + 1;
+    const uint32_t f0n = (f0 <= 4096) ? (uint32_t)f0 : 0u;
+    fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::kWalkThreads, (size_t)f0n * 8, s>>>(
+        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n);
     ++g_launches;
     return cuda_check("k5_walk");
 }

@@ -993,8 +993,10 @@ __global__ void __launch_bounds__(256) k3_fill_grid(Gens G, int L, uint64_t top,
 // subtree: F_j(a) = Tb[j][r - a g_j] = units with a'_j >= a under the current
 // prefix.  At each level a_j = max{a : F_j(a) > R}, then R -= F_j(a_j + 1).
 // Returns the remaining R (offset inside the memo block for S; 0 for W).
+// F0 (optional, shared memory): F0[a] = Tb_0[n - a g_0] for a <= n / g_0, the level-0 column of the
+// search, so the first (widest) level costs shared-memory probes instead of L2 round trips.
 __device__ uint64_t unrank(const uint64_t *__restrict__ Tb, uint64_t top, const Gens &G, int L, uint64_t n,
-                           uint64_t R, uint32_t *a)
+                           uint64_t R, uint32_t *a, const uint64_t *F0 = nullptr)
 {
     const int lane = threadIdx.x & 31;
     uint64_t r = n;
@@ -1002,11 +1004,12 @@ __device__ uint64_t unrank(const uint64_t *__restrict__ Tb, uint64_t top, const 
         const uint64_t *Tj = Tb + (uint64_t)j * top;
         const uint64_t gj = G.g[j];
         const uint64_t amax = r / gj;
+        const bool cached = (j == 0) && F0 != nullptr;
         uint64_t lo = 0, hi = amax;
         while (lo < hi) {
             const uint64_t step = (hi - lo + 31) / 32;
             const uint64_t cand = lo + (uint64_t)(lane + 1) * step;
-            const bool pred = cand <= hi && __ldg(Tj + (r - cand * gj)) > R;
+            const bool pred = cand <= hi && (cached ? F0[cand] : __ldg(Tj + (r - cand * gj))) > R;
             const unsigned bal = __ballot_sync(kFull, pred);
             const int m = __popc(bal);
             const uint64_t nlo = lo + (uint64_t)m * step;
@@ -1016,7 +1019,7 @@ __device__ uint64_t unrank(const uint64_t *__restrict__ Tb, uint64_t top, const 
             hi = nhi;
         }
         a[j] = (uint32_t)lo;
-        const uint64_t fnext = (lo + 1 <= amax) ? __ldg(Tj + (r - (lo + 1) * gj)) : 0;
+        const uint64_t fnext = (lo + 1 <= amax) ? (cached ? F0[lo + 1] : __ldg(Tj + (r - (lo + 1) * gj))) : 0;
         R -= fnext;
         r -= lo * gj;
     }
@@ -1169,8 +1172,12 @@ struct WalkTables {
 template <int D, int T, int MODE>
 __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
-                                                         uint32_t *out, uint64_t out_cap_rows, uint64_t row_base)
+                                                         uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
+                                                         uint32_t f0n)
 {
+    extern __shared__ uint64_t f0s[];   // level-0 unrank column (f0n entries, 0 = not cached)
+    for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Tb + (n64 - (uint64_t)q * G.g[0]));
+    if (f0n) __syncthreads();
     constexpr int L = D - T;
     static_assert(L >= 1, "at least one leading coordinate");
     __shared__ BlockInfo binfo[kWalkThreads / 32][32];
@@ -1206,7 +1213,7 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
         sl.len = (shard_len - sl.begin) < slice_len ? (shard_len - sl.begin) : slice_len;
         {
             uint32_t ua[kMaxD];
-            const uint64_t k0 = unrank(Tb, top, G, L, n64, shard_begin + sl.begin, ua);
+            const uint64_t k0 = unrank(Tb, top, G, L, n64, shard_begin + sl.begin, ua, f0n ? f0s : nullptr);
             sl.k0 = (MODE == FZ_COUNT) ? 0 : k0;
 #pragma unroll
             for (int j = 0; j < L; ++j) sl.a[j] = ua[j];
