@@ -372,15 +372,19 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t nthreads)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// Progress flags between the ring-fill workers and its helper warp: shared-memory atomics with
+// acquire / release ordering (atomics, so compute-sanitizer racecheck sees the synchronisation).
 __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t *p)
 {
     uint32_t v;
-    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    asm volatile("atom.acquire.cta.shared::cta.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(smem_addr(p)) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release_cta(uint32_t *p, uint32_t v)
 {
-    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+    asm volatile("{\n\t.reg .b32 old;\n\tatom.release.cta.shared::cta.exch.b32 old, [%0], %1;\n\t}" ::"r"(smem_addr(p)),
+                 "r"(v)
+                 : "memory");
 }
 
 // Fill mode 1: one CTA runs the elementwise batches in order;

@@ -1,0 +1,30 @@
+"""Small GPU workload for compute-sanitizer: every fill mode, every K5 mode, t = 0 / d, shards."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+from paper_2407_20474_b200 import fz  # noqa: E402
+
+C = O.C()
+cases = [((13, 37, 38, 40), 800, 2), ((6, 9, 20), 300, 2), ((3, 5, 8, 11), 200, 3), ((7, 7, 3), 150, 1),
+         ((13, 37, 38, 40, 41), 600, 3), ((5,), 40, 0), ((6, 9, 20), 120, 3)]
+bad = 0
+for fill in (0, 1, 2, 3, 4, 5):
+    fz.set_fill_mode(fill)
+    for g, n, t in cases:
+        memo = fz.memo_build(g, t, n + 1)
+        want, cnt, h = C.enumerate(n, g)
+        for ns in (1, 3):
+            got, hs = [], 0
+            for s in range(ns):
+                out, r, _ = fz.enumerate(memo, n, "materialize", shard=s, nshards=ns)
+                got.append(out.cpu().numpy().view(np.uint32).reshape(-1, len(g))[:r])
+                hs = (hs + fz.enumerate(memo, n, "hash", shard=s, nshards=ns)[2]) % (1 << 64)
+            ok = np.array_equal(np.concatenate(got), want.reshape(-1, len(g))) and hs == h
+            ok = ok and fz.enumerate(memo, n, "count")[1] == cnt
+            bad += (not ok)
+fz.set_fill_mode(0)
+print("sanitize subset:", "OK" if bad == 0 else f"{bad} FAILURES")
