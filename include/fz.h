@@ -70,7 +70,12 @@ typedef struct {
                                4 = one pass per tail dimension, residue chains stepped in order;
                                5 = one pass per tail dimension, chains in unrolled (scan) form */
     uint64_t window_rows;   /* max rows a batch and its look-back window span (ring size needed) */
+    uint64_t memo_top;      /* memo ROWS cover x < memo_top <= top (topOfMemo); the count
+                               tables cover x < top.  memo_top < top is a partial memo */
 } fz_memo_info;
+
+#define FZ_MEMO_TOP_AUTO 0ull           /* fz_layout_create_partial: largest memo_top whose rows fit the cap */
+#define FZ_MEMO_TOP_FULL UINT64_MAX     /* fz_layout_create_partial: memo_top = top (full memo) */
 
 /* ---------------------------------------------------------------- A1 -- */
 /* Validate (gens, d, t, top) and return the device workspace bytes
@@ -99,6 +104,17 @@ void fz_set_fill_mode(int mode);
 typedef struct fz_layout fz_layout;
 fz_status fz_layout_create(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out);
 fz_status fz_layout_workspace_bytes(const fz_layout *lay, uint64_t *bytes);
+
+/* Partial memo (topOfMemo; "excepting dimension 3"):
+ * count tables for every x < top (so any n < top can be planned and counted), memo ROWS only for
+ * x < memo_top (1 <= memo_top <= top; FZ_MEMO_TOP_AUTO = the largest memo_top whose rows fit the memo
+ * cap; FZ_MEMO_TOP_FULL = top).  Enumerating n >= memo_top (MATERIALIZE / HASH) walks into the tail
+ * coordinates wherever the remainder has no memo block and copies the memo suffix blocks
+ * Z_{>=k}(x), x < memo_top, below it (k5_deep; reading R19): the same rows in the same order
+ * as the full memo.  COUNT needs the count tables only.  memo_top is forced to top when t = 0 or
+ * with_entries = 0.  Errors as fz_layout_create, plus FZ_EINVAL for memo_top > top (other than FULL). */
+fz_status fz_layout_create_partial(const uint32_t *gens, int d, int t, uint64_t top, uint64_t memo_top,
+                                   int with_entries, fz_layout **out);
 void fz_layout_free(fz_layout *lay);
 
 /* Memo-dimension recommendation (PAPER.md:301 observes that the best memoDim
@@ -216,7 +232,9 @@ fz_status fz_enumerate(const fz_memo *m, uint64_t n, fz_mode mode, int shard, in
  * and for MATERIALIZE stream the rows back into the HOST buffer h_out
  * (u32[rows * d]; pinned memory recommended) in chunks that overlap the
  * device-to-host copies with the enumeration (Buffer ->
- * host).  d_ws must hold fz_run_workspace_bytes.  Synchronises `stream`. */
+ * host).  d_ws must hold fz_run_workspace_bytes.  When the full memo would exceed the memo cap the
+ * memo is partial (memo_top = FZ_MEMO_TOP_AUTO) instead of FZ_ECAP.
+ * Synchronises `stream`. */
 fz_status fz_run_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, uint64_t *bytes);
 fz_status fz_run_host(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, void *d_ws, uint64_t ws_bytes,
                       uint32_t *h_out, uint64_t h_out_capacity_rows, void *stream, uint64_t *rows_out,

@@ -117,6 +117,7 @@ struct Layout {
 struct Sizing {
     int d, t, L;
     uint64_t top;
+    uint64_t ltop = 0;   // memo rows cover x < ltop <= top (topOfMemo); tables cover x < top
     uint64_t entries = 0, max_card = 0, window = 0, ring_rows = 0, batches = 0;
     uint32_t batch = 0;
     uint32_t stage_words = 0;   // fill mode 1: words per TMA link chunk buffer
@@ -146,7 +147,9 @@ fz_status validate(const uint32_t *g, int d, int t, uint64_t top)
     return FZ_OK;
 }
 
-fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entries, const HostTables &H, Sizing &z)
+// memo_top: FZ_MEMO_TOP_FULL (= top), FZ_MEMO_TOP_AUTO (the largest that fits the cap), or 1..top.
+fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo_top, int with_entries,
+                    const HostTables &H, Sizing &z)
 {
     z.d = d;
     z.t = t;
@@ -154,8 +157,21 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
     z.top = top;
     const int L = z.L;
     const uint64_t *card = H.S.data() + (size_t)L * top;
+    if (!with_entries || t == 0 || memo_top == FZ_MEMO_TOP_FULL) {
+        memo_top = top;
+    } else if (memo_top == FZ_MEMO_TOP_AUTO) {   // partial memo: longest prefix of x whose rows fit the cap
+        const uint64_t cap_rows = g_memo_cap / (4ull * t);
+        uint64_t e = 0, x = 0;
+        while (x < top && e + card[x] <= cap_rows) e += card[x++];
+        if (x == 0) return fail(FZ_ECAP, "even Memo[0] exceeds the memo cap");
+        memo_top = x;
+    } else if (memo_top > top) {
+        return fail(FZ_EINVAL, "memo_top=%llu > top=%llu", (unsigned long long)memo_top, (unsigned long long)top);
+    }
+    z.ltop = memo_top;
+    const uint64_t ltop = memo_top;
     uint64_t entries = 0, mx = 0;
-    for (uint64_t x = 0; x < top; ++x) {
+    for (uint64_t x = 0; x < ltop; ++x) {
         if (__builtin_add_overflow(entries, card[x], &entries)) return fail(FZ_ERANGE, "memo entries exceed 2^64");
         mx = std::max(mx, card[x]);
     }
@@ -169,13 +185,13 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
     }
     if (t == 0) b = 1;
     z.batch = b;
-    z.batches = (top + b - 1) / b;
+    z.batches = (ltop + b - 1) / b;
     // live window of the recurrence: rows of [x0 - hmax, x0 + b) for every batch start x0
-    std::vector<uint64_t> off(top + 1, 0);
-    for (uint64_t x = 0; x < top; ++x) off[x + 1] = off[x] + card[x];
+    std::vector<uint64_t> off(ltop + 1, 0);
+    for (uint64_t x = 0; x < ltop; ++x) off[x + 1] = off[x] + card[x];
     uint64_t win = 0;
-    for (uint64_t x0 = 0; x0 < top; x0 += b) {
-        uint64_t lo = x0 > hmax ? x0 - hmax : 0, hi = std::min<uint64_t>(x0 + b, top);
+    for (uint64_t x0 = 0; x0 < ltop; x0 += b) {
+        uint64_t lo = x0 > hmax ? x0 - hmax : 0, hi = std::min<uint64_t>(x0 + b, ltop);
         win = std::max(win, off[hi] - off[lo]);
     }
     z.window = win;
@@ -189,12 +205,12 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
         // (look-back window + the batch whose bulk store may still be reading), links in chunks of chb batches
         // ring: rows of [x0 - max(hmax, (Q+1) b), x0 + b) for every batch (look-back window + batches whose
         // bulk store may still be pending); links in chunks of chb batches.  Largest Q, chb that fit.
-        auto boffv = [&](uint64_t k) { return off[std::min<uint64_t>(k * b, top)]; };
+        auto boffv = [&](uint64_t k) { return off[std::min<uint64_t>(k * b, ltop)]; };
         auto ring_for = [&](uint64_t Q) {
             uint64_t win2 = 0;
             const uint64_t back = std::max<uint64_t>((uint64_t)hmax, (Q + 1) * b);
-            for (uint64_t x0 = 0; x0 < top; x0 += b) {
-                uint64_t lo = x0 > back ? x0 - back : 0, hi = std::min<uint64_t>(x0 + b, top);
+            for (uint64_t x0 = 0; x0 < ltop; x0 += b) {
+                uint64_t lo = x0 > back ? x0 - back : 0, hi = std::min<uint64_t>(x0 + b, ltop);
                 win2 = std::max<uint64_t>(win2, off[hi] - off[lo]);
             }
             uint64_t ring = 4;
@@ -230,7 +246,7 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
         for (int i = 0; i + 1 < t; ++i) {
             const uint64_t *Si = H.S.data() + (size_t)(L + i) * top, *Si1 = Si + top;
             uint64_t mb = 0;
-            for (uint64_t x = 0; x < top; ++x) mb = std::max<uint64_t>(mb, Si[x] - Si1[x]);
+            for (uint64_t x = 0; x < ltop; ++x) mb = std::max<uint64_t>(mb, Si[x] - Si1[x]);
             z.level_block[i] = mb;
             if (3ull * 512 * 4 * t + mb * 4ull * t + 6 * 1024 + 16 > kSmemMax) chains_fit = false;
         }
@@ -239,13 +255,15 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, int with_entr
         for (int i = 0; i + 1 < t; ++i) {
             const uint64_t *Si = H.S.data() + (size_t)(L + i) * top;
             uint64_t mx = 0;
-            for (uint64_t x = 0; x < top; ++x) mx = std::max<uint64_t>(mx, Si[x]);
+            for (uint64_t x = 0; x < ltop; ++x) mx = std::max<uint64_t>(mx, Si[x]);
             z.list_cap = std::max<uint64_t>(z.list_cap, mx);
-            chains_max = std::max<uint64_t>(chains_max, std::min<uint64_t>(g[L + i], top));
+            chains_max = std::max<uint64_t>(chains_max, std::min<uint64_t>(g[L + i], ltop));
         }
         z.list_bytes = chains_max * z.list_cap * 4ull * t;
         const int forced = g_fill_override;
-        if (forced >= 1 && forced <= 5 && !(forced == 1 && !fit) && !(forced == 4 && !chains_fit))
+        // modes 1-4 fill the whole table range; a partial memo (ltop < top) takes mode 5
+        if (forced >= 1 && forced <= 5 && !(forced == 1 && !fit) && !(forced == 4 && !chains_fit) &&
+            (ltop == top || forced == 5))
             z.fill_mode = forced;
         else
             z.fill_mode = 5;
@@ -340,15 +358,15 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
     if (z.fill_mode == 5) {
         const uint32_t h_last = m->lay->g[z.d - 1];
         const unsigned blocks = (unsigned)std::min<uint64_t>((z.top + 255) / 256, (uint64_t)device_sms() * 8);
-        fzk::k3_last_level<T><<<std::max(blocks, 1u), 256, 0, s>>>(m->S, m->off, m->rows, z.top, z.L, h_last);
+        fzk::k3_last_level<T><<<std::max(blocks, 1u), 256, 0, s>>>(m->S, m->off, m->rows, z.top, z.ltop, z.L, h_last);
         ++g_launches;
         fz_status st = cuda_check("k3_last_level");
         const unsigned wblocks = (unsigned)std::min<uint64_t>((z.top * 32 + 255) / 256, (uint64_t)device_sms() * 16);
         uint32_t *list = (uint32_t *)(m->ws + z.lay.list);
         for (int i = T - 2; i >= 0 && !st; --i) {
             const uint32_t h = m->lay->g[z.L + i];
-            fzk::k3_scan_a<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.L, i, h);
-            fzk::k3_scan_b<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.L, i, h);
+            fzk::k3_scan_a<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.ltop, z.L, i, h);
+            fzk::k3_scan_b<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.ltop, z.L, i, h);
             g_launches += 2;
             st = cuda_check("k3_scan");
         }
@@ -357,7 +375,7 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
     if (z.fill_mode == 4) {
         const uint32_t h_last = m->lay->g[z.d - 1];
         const unsigned blocks = (unsigned)std::min<uint64_t>((z.top + 255) / 256, (uint64_t)device_sms() * 8);
-        fzk::k3_last_level<T><<<std::max(blocks, 1u), 256, 0, s>>>(m->S, m->off, m->rows, z.top, z.L, h_last);
+        fzk::k3_last_level<T><<<std::max(blocks, 1u), 256, 0, s>>>(m->S, m->off, m->rows, z.top, z.ltop, z.L, h_last);
         ++g_launches;
         fz_status st = cuda_check("k3_last_level");
         for (int i = T - 2; i >= 0 && !st; --i) {
@@ -507,6 +525,67 @@ fz_status launch_table(int d, int mode, const WalkArgs &a, const uint64_t *off, 
     }
 }
 
+template <int D, int T>
+fz_status launch_deep_dt(int mode, const WalkArgs &a, const uint64_t *S, uint64_t ltop, const uint64_t *off,
+                         cudaStream_t s)
+{
+    auto kern = (mode == FZ_MATERIALIZE) ? fzk::k5_deep<D, T, FZ_MATERIALIZE> : fzk::k5_deep<D, T, FZ_HASH>;
+    static thread_local int per_sm[2] = {0, 0};
+    int &ps = per_sm[mode == FZ_MATERIALIZE ? 0 : 1];
+    if (!ps) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, fzk::kWalkThreads, 0) != cudaSuccess || ps < 1)
+            ps = 2;
+        ps = std::min(ps, 8);
+    }
+    // closed form of the last two coordinates (PROG leaves): Z(x; g, h), g = g_{d-2}, h = g_{d-1}
+    fzk::ProgGens P{1, 1, 1, 1, 1, 0};
+    if (D >= 2) {
+        const uint32_t g = a.G.g[D >= 2 ? D - 2 : 0], h = a.G.g[D - 1];
+        uint32_t x = g, y = h;
+        while (y) { const uint32_t t = x % y; x = y; y = t; }
+        P.g = g;
+        P.h = h;
+        P.e = x;
+        P.g1 = g / x;
+        P.h1 = h / x;
+        // inverse of g1 mod h1 (extended Euclid; 0 when h1 = 1)
+        int64_t r0 = P.h1, r1 = P.g1 % P.h1, s0 = 0, s1 = 1;
+        while (r1) {
+            const int64_t q = r0 / r1, r2 = r0 - q * r1, s2 = s0 - q * s1;
+            r0 = r1; r1 = r2; s0 = s1; s1 = s2;
+        }
+        P.inv = P.h1 == 1 ? 0u : (uint32_t)(((s0 % (int64_t)P.h1) + P.h1) % P.h1);
+    }
+    kern<<<(unsigned)(device_sms() * ps), fzk::kWalkThreads, 0, s>>>(a.G, a.n, a.hdr, S, a.top, ltop, off, a.wt.memo,
+                                                                      a.out, a.cap, a.row_base, P);
+    ++g_launches;
+    return cuda_check("k5_deep");
+}
+
+template <int D, int T = 1>
+fz_status launch_deep_d(int t, int mode, const WalkArgs &a, const uint64_t *S, uint64_t ltop, const uint64_t *off,
+                        cudaStream_t s)
+{
+    if constexpr (T <= D) {
+        if (t == T) return launch_deep_dt<D, T>(mode, a, S, ltop, off, s);
+        return launch_deep_d<D, T + 1>(t, mode, a, S, ltop, off, s);
+    } else {
+        return fail(FZ_EINVAL, "t=%d not instantiated for d=%d", t, D);
+    }
+}
+
+template <int D = 1>
+fz_status launch_deep(int d, int t, int mode, const WalkArgs &a, const uint64_t *S, uint64_t ltop,
+                      const uint64_t *off, cudaStream_t s)
+{
+    if constexpr (D <= FZ_MAX_D) {
+        if (d == D) return launch_deep_d<D>(t, mode, a, S, ltop, off, s);
+        return launch_deep<D + 1>(d, t, mode, a, S, ltop, off, s);
+    } else {
+        return fail(FZ_EINVAL, "d=%d not instantiated", d);
+    }
+}
+
 // host-side rank / unrank over the layout's host tables (fz_shard_rows, fz_run_host)
 uint64_t host_row_rank(const fz_layout *lay, uint64_t n, const uint32_t *a)
 {
@@ -560,7 +639,8 @@ void host_shard(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, int
     }
 }
 
-fz_status make_layout(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out)
+fz_status make_layout(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out,
+                      uint64_t memo_top = FZ_MEMO_TOP_FULL)
 {
     *out = nullptr;
     fz_status st = validate(gens, d, t, top);
@@ -570,7 +650,7 @@ fz_status make_layout(const uint32_t *gens, int d, int t, uint64_t top, int with
     for (int i = 0; i < d; ++i) lay->g[i] = gens[i];
     lay->with_entries = with_entries ? 1 : 0;
     if ((st = host_tables(gens, d, d - t, top, lay->H)) ||
-        (st = size_memo(gens, d, t, top, with_entries, lay->H, lay->z))) {
+        (st = size_memo(gens, d, t, top, memo_top, with_entries, lay->H, lay->z))) {
         delete lay;
         return st;
     }
@@ -592,6 +672,14 @@ fz_status fz_layout_create(const uint32_t *gens, int d, int t, uint64_t top, int
 {
     if (!out) return fail(FZ_EINVAL, "out is NULL");
     return make_layout(gens, d, t, top, with_entries, out);
+}
+
+fz_status fz_layout_create_partial(const uint32_t *gens, int d, int t, uint64_t top, uint64_t memo_top,
+                                   int with_entries, fz_layout **out)
+{
+    if (!out) return fail(FZ_EINVAL, "out is NULL");
+    if (memo_top == FZ_MEMO_TOP_FULL) memo_top = top;
+    return make_layout(gens, d, t, top, with_entries, out, memo_top);
 }
 
 void fz_layout_free(fz_layout *lay) { delete lay; }
@@ -616,6 +704,7 @@ fz_status fz_layout_get_info(const fz_layout *lay, fz_memo_info *info)
     info->batch = z.batch;
     info->fill_mode = z.fill_mode;
     info->window_rows = z.window;
+    info->memo_top = z.ltop;
     return FZ_OK;
 }
 
@@ -670,6 +759,7 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
     tb.chunk = m->chunk;
     tb.links = m->links;
     tb.top = z.top;
+    tb.ltop = z.ltop;
     tb.m = z.L > 0 ? lay->g[z.L - 1] : 1;
     tb.R = (z.top + tb.m - 1) / tb.m;
     tb.d = z.d;
@@ -926,6 +1016,8 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
     a.out = d_out;
     a.cap = (p->mode == FZ_MATERIALIZE) ? out_capacity_rows : ~0ull;
     a.row_base = row_base;
+    if (p->mode != FZ_COUNT && z.t > 0 && p->n >= z.ltop)   // partial memo: Memo[p] missing for p >= ltop
+        return launch_deep(z.d, z.t, (int)p->mode, a, m->S, z.ltop, m->off, (cudaStream_t)stream);
     if (z.L == 0) return launch_table(z.d, (int)p->mode, a, m->off, (cudaStream_t)stream);
     return launch_walk(z.d, z.t, (int)p->mode, a, (cudaStream_t)stream);
 }
@@ -972,7 +1064,7 @@ fz_status fz_run_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t n,
 {
     if (!bytes) return fail(FZ_EINVAL, "bytes is NULL");
     fz_layout *lay = nullptr;
-    fz_status st = make_layout(gens, d, t, n + 1, mode != FZ_COUNT, &lay);
+    fz_status st = make_layout(gens, d, t, n + 1, mode != FZ_COUNT, &lay, FZ_MEMO_TOP_AUTO);
     if (st) return st;
     const uint64_t rows = lay->H.S[n];
     const int chunks = (mode == FZ_MATERIALIZE) ? kRunChunks : 1;
@@ -988,7 +1080,7 @@ fz_status fz_run_host(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mo
 {
     if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode");
     fz_layout *lay = nullptr;
-    fz_status st = make_layout(gens, d, t, n + 1, mode != FZ_COUNT, &lay);
+    fz_status st = make_layout(gens, d, t, n + 1, mode != FZ_COUNT, &lay, FZ_MEMO_TOP_AUTO);
     if (st) return st;
     const uint64_t rows_total = lay->H.S[n];
     const int chunks = (mode == FZ_MATERIALIZE) ? kRunChunks : 1;

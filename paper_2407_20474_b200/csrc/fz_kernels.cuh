@@ -80,7 +80,8 @@ struct Tables {
     uint64_t *offT;     // top, residue-major
     uint64_t *chunk;    // gridDim scratch for the offset scan
     void *links;        // entries (u32 ring links or u64 row links), or nullptr
-    uint64_t top;
+    uint64_t top;       // tables cover x < top
+    uint64_t ltop;      // memo rows cover x < ltop <= top (topOfMemo; partial memo when < top)
     uint32_t m;         // g_L
     uint64_t R;         // rows per residue column = ceil(top / m)
     int d, L, t;
@@ -243,7 +244,7 @@ __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigne
         }
         if (p == pa) {   // K2 stage A: chunk sums of card
             uint64_t s = 0;
-            for (uint64_t x = c0 + threadIdx.x; x < c1; x += blockDim.x) s += __ldcg(card + x);
+            for (uint64_t x = c0 + threadIdx.x; x < c1 && x < tb.ltop; x += blockDim.x) s += __ldcg(card + x);
             uint64_t tot;
             block_excl_scan(s, sm, &tot);
             if (threadIdx.x == 0) tb.chunk[blockIdx.x] = tot;
@@ -257,13 +258,14 @@ __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigne
             const uint64_t m = tb.m;
             for (uint64_t xb = c0; xb < c1; xb += blockDim.x) {
                 const uint64_t x = xb + threadIdx.x;
-                const uint64_t v = x < c1 ? __ldcg(card + x) : 0;
+                const uint64_t c = x < c1 ? __ldcg(card + x) : 0;
+                const uint64_t v = x < tb.ltop ? c : 0;   // CSR over the memo's rows only (x < ltop)
                 uint64_t t2;
                 const uint64_t ex = pre + block_excl_scan(v, sm, &t2);
                 if (x < c1) {
                     tb.off[x] = ex;
                     const uint64_t ti = (x % m) * tb.R + x / m;
-                    tb.cardT[ti] = (uint32_t)v;
+                    tb.cardT[ti] = (uint32_t)c;
                     tb.offT[ti] = ex;
                     if (x + 1 == top) tb.off[top] = ex + v;
                 }
@@ -582,11 +584,11 @@ __global__ void __launch_bounds__(1024) k3_fill_ring(const uint64_t *__restrict_
 // last tail dimension: block t-1 of Z(x) = [(0,..,0, x/h)] if h | x (x = 0 gives Memo[0] = [0])
 template <int T>
 __device__ __forceinline__ void last_level_body(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
-                                                uint32_t *rows, uint64_t top, int L, uint32_t h, uint64_t gt,
-                                                uint64_t ng)
+                                                uint32_t *rows, uint64_t top, uint64_t ltop, int L, uint32_t h,
+                                                uint64_t gt, uint64_t ng)
 {
     const uint64_t *Sl = S + (uint64_t)(L + T - 1) * top;
-    for (uint64_t x = gt; x < top; x += ng) {
+    for (uint64_t x = gt; x < ltop; x += ng) {
         if (x % h) continue;
         const uint64_t dst = __ldcg(off + x + 1) - __ldcg(Sl + x);
         uint32_t *o = rows + dst * T;
@@ -598,10 +600,10 @@ __device__ __forceinline__ void last_level_body(const uint64_t *__restrict__ S, 
 
 template <int T>
 __global__ void __launch_bounds__(256) k3_last_level(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
-                                                      uint32_t *rows, uint64_t top, int L, uint32_t h)
+                                                      uint32_t *rows, uint64_t top, uint64_t ltop, int L, uint32_t h)
 {
     const uint64_t *Sl = S + (uint64_t)(L + T - 1) * top;
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < top; x += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < ltop; x += (uint64_t)gridDim.x * blockDim.x) {
         if (x % h) continue;
         const uint64_t dst = __ldg(off + x + 1) - __ldg(Sl + x);
         uint32_t *o = rows + dst * T;
@@ -793,11 +795,11 @@ __global__ void __launch_bounds__(512) k3_chain(const uint64_t *__restrict__ S, 
 template <int T>
 __device__ __forceinline__ void scan_a_body(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                             const uint32_t *rows, uint32_t *list, uint64_t cap_list, uint64_t top,
-                                            int L, int i, uint32_t h, uint64_t gw, uint64_t nw)
+                                            uint64_t ltop, int L, int i, uint32_t h, uint64_t gw, uint64_t nw)
 {
     const int lane = threadIdx.x & 31;
     const uint64_t *Si = S + (uint64_t)(L + i) * top, *Si1 = Si + top;
-    for (uint64_t x = gw; x + h < top; x += nw) {
+    for (uint64_t x = gw; x + h < ltop; x += nw) {
         const uint64_t ns = __ldg(Si1 + x);
         if (ns == 0) continue;
         const uint64_t so = __ldg(off + x + 1) - ns, base = __ldg(Si + x) - ns;
@@ -814,11 +816,11 @@ __device__ __forceinline__ void scan_a_body(const uint64_t *__restrict__ S, cons
 template <int T>
 __device__ __forceinline__ void scan_b_body(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                             uint32_t *rows, const uint32_t *list, uint64_t cap_list, uint64_t top,
-                                            int L, int i, uint32_t h, uint64_t gw, uint64_t nw)
+                                            uint64_t ltop, int L, int i, uint32_t h, uint64_t gw, uint64_t nw)
 {
     const int lane = threadIdx.x & 31;
     const uint64_t *Si = S + (uint64_t)(L + i) * top, *Si1 = Si + top;
-    for (uint64_t x = h + gw; x < top; x += nw) {
+    for (uint64_t x = h + gw; x < ltop; x += nw) {
         const uint64_t si = __ldg(Si + x);
         const uint64_t nb = si - __ldg(Si1 + x);
         if (nb == 0) continue;
@@ -845,18 +847,18 @@ __device__ __forceinline__ void scan_b_body(const uint64_t *__restrict__ S, cons
 template <int T>
 __global__ void __launch_bounds__(256) k3_scan_a(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                                   const uint32_t *rows, uint32_t *list, uint64_t cap_list, uint64_t top,
-                                                  int L, int i, uint32_t h)
+                                                  uint64_t ltop, int L, int i, uint32_t h)
 {
-    scan_a_body<T>(S, off, rows, list, cap_list, top, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
+    scan_a_body<T>(S, off, rows, list, cap_list, top, ltop, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
                    ((uint64_t)gridDim.x * blockDim.x) >> 5);
 }
 
 template <int T>
 __global__ void __launch_bounds__(256) k3_scan_b(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                                   uint32_t *rows, const uint32_t *list, uint64_t cap_list, uint64_t top,
-                                                  int L, int i, uint32_t h)
+                                                  uint64_t ltop, int L, int i, uint32_t h)
 {
-    scan_b_body<T>(S, off, rows, list, cap_list, top, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
+    scan_b_body<T>(S, off, rows, list, cap_list, top, ltop, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
                    ((uint64_t)gridDim.x * blockDim.x) >> 5);
 }
 
@@ -873,13 +875,13 @@ __global__ void __launch_bounds__(1024) k1_memo(Gens G, Tables tb, unsigned int 
     const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
     grid_barrier(counter, target);
-    last_level_body<T>(tb.S, tb.off, rows, tb.top, tb.L, G.g[tb.d - 1], gt, ng);
+    last_level_body<T>(tb.S, tb.off, rows, tb.top, tb.ltop, tb.L, G.g[tb.d - 1], gt, ng);
     for (int i = T - 2; i >= 0; --i) {
         const uint32_t h = G.g[tb.L + i];
         grid_barrier(counter, target);
-        scan_a_body<T>(tb.S, tb.off, rows, list, cap_list, tb.top, tb.L, i, h, gt >> 5, ng >> 5);
+        scan_a_body<T>(tb.S, tb.off, rows, list, cap_list, tb.top, tb.ltop, tb.L, i, h, gt >> 5, ng >> 5);
         grid_barrier(counter, target);
-        scan_b_body<T>(tb.S, tb.off, rows, list, cap_list, tb.top, tb.L, i, h, gt >> 5, ng >> 5);
+        scan_b_body<T>(tb.S, tb.off, rows, list, cap_list, tb.top, tb.ltop, tb.L, i, h, gt >> 5, ng >> 5);
     }
 }
 
@@ -1397,6 +1399,260 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
     if constexpr (MODE == FZ_HASH) {
         acc_hash = warp_sum_u64(acc_hash);
         if (lane == 0) atomicAdd((unsigned long long *)(result + 1), (unsigned long long)acc_hash);
+    }
+}
+
+// ------------------------------------------------- K5, partial memo (f2)
+// topOfMemo = ltop <= n: remainders p >= ltop have no memo
+// block.  The paper's Else branch then walks the tail coordinates with plain nextCandidate steps;
+// here the walk is a depth-first traversal of the prefix tree in descending lex order.  A node at
+// depth k (a_0..a_k fixed, remainder x = n - phi(a_0..a_k)) is a LEAF BLOCK when
+//   PROG:   k = d-3: its rows Z(x; g_{d-2}, g_{d-1}) are an arithmetic progression, in closed form
+//           (a_{d-2} = w_0 - j h', a_{d-1} = l_0 + j g'; g' = g_{d-2}/e, h' = g_{d-1}/e, e = gcd);
+//   DIRECT: k = d-2 (d = 2, or a walk started there): at most the row (.., x / g_{d-1});
+//   MEMO:   k >= L-1 and x < ltop: the suffix Z_{>=k+1}(x) of Memo[x] (its last S_{k+1}[x] rows, whose
+//           coordinates L..k are zero), with a_L..a_k written over them.
+// Other nodes are descended; empty subtrees (S = 0) are skipped, and a node whose remaining children
+// hold no rows is left at once.  Same rows in the same order as the full-memo walk and as Alg 5
+// with topOfMemo (reading R19).  Per warp: the 32 lanes evaluate 32 consecutive children of the
+// current node; the leaf blocks before the first child that must be descended are copied with the
+// flattened block copy of k5_walk, then the walk descends into that child, moves to the next 32
+// siblings, or backs up.
+template <int N>
+__device__ __forceinline__ uint64_t sel_u64(const uint64_t (&v)[N], int k)
+{
+    uint64_t x = 0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+        if (j == k) x = v[j];
+    return x;
+}
+
+template <int N>
+__device__ __forceinline__ uint32_t sel_u32(const uint32_t (&v)[N], int k)
+{
+    uint32_t x = 0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+        if (j == k) x = v[j];
+    return x;
+}
+
+// BlockInfo.memo_row of a computed leaf: flag bits, then two 30-bit coordinates
+constexpr uint64_t kComputed = 1ull << 63, kProg = 1ull << 62;
+
+struct ProgGens {     // closed form of Z(x; g, h), g = g_{d-2}, h = g_{d-1}
+    uint32_t g, h, e, g1, h1, inv;   // e = gcd(g, h), g1 = g/e, h1 = h/e, inv = g1^{-1} mod h1
+};
+
+// Z(x; g, h) in descending lex order: rows (w0 - j h1, l0 + j g1), j < count
+__device__ __forceinline__ uint32_t prog_block(const ProgGens &P, uint32_t x, uint32_t &w0, uint32_t &l0)
+{
+    if (x % P.e) return 0;
+    const uint32_t ws = (uint32_t)(((uint64_t)((x / P.e) % P.h1) * P.inv) % P.h1);   // w == ws (mod h1)
+    const uint32_t wmax = x / P.g;
+    if (wmax < ws) return 0;
+    w0 = wmax - (wmax - ws) % P.h1;
+    l0 = (x - w0 * P.g) / P.h;
+    return w0 / P.h1 + 1;
+}
+
+template <int D, int T, int MODE>
+__global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, PlanHdr *hdr,
+                                                        const uint64_t *__restrict__ S, uint64_t top, uint64_t ltop,
+                                                        const uint64_t *__restrict__ off,
+                                                        const uint32_t *__restrict__ memo, uint32_t *out,
+                                                        uint64_t out_cap_rows, uint64_t row_base, ProgGens P)
+{
+    constexpr int L = D - T;
+    static_assert(T >= 1 && MODE != FZ_COUNT, "partial walk: rows of a memo with t >= 1");
+    __shared__ BlockInfo binfo[kWalkThreads / 32][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t nslices = hdr->nslices, slice_len = hdr->slice_len, shard_begin = hdr->shard_begin,
+                   shard_len = hdr->shard_len;
+    if (MODE == FZ_MATERIALIZE && hdr->rows > out_cap_rows) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) hdr->err = 1;
+        return;
+    }
+    if (row_base == ~0ull) row_base = hdr->row_begin;
+    uint64_t acc_rows = 0, acc_hash = 0;
+    BlockInfo *bi = binfo[wib];
+    const uint32_t hl = G.g[D - 1];
+    for (;;) {
+        uint64_t s = 0;
+        if (lane == 0) s = atomicAdd(&hdr->next_slice, 1ull);
+        s = shfl_u64(s, 0);
+        if (s >= nslices) break;
+        const uint64_t begin = s * slice_len;
+        uint64_t left = (shard_len - begin) < slice_len ? (shard_len - begin) : slice_len;
+        uint64_t outpos = begin;
+        // the slice's first row, all d coordinates (the S tables cover every x <= n)
+        uint32_t a[D];
+        uint64_t r[D + 1];
+        {
+            uint32_t ua[kMaxD];
+            unrank(S, top, G, D, n64, shard_begin + begin, ua);
+#pragma unroll
+            for (int j = 0; j < D; ++j) a[j] = ua[j];
+        }
+        r[0] = n64;
+#pragma unroll
+        for (int j = 0; j < D; ++j) r[j + 1] = r[j] - (uint64_t)a[j] * G.g[j];
+        // the leaf holding this row (same rules as the walk below)
+        int k = 0;
+        while (!(k + 3 == D || k + 2 == D || (k + 1 >= L && sel_u64(r, k + 1) < ltop))) ++k;
+        // offset of the row inside its leaf: its rank over coordinates k+1..d-1
+        uint64_t kfirst = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            if (j <= k) continue;
+            const uint64_t nxt = ((uint64_t)a[j] + 1) * G.g[j];
+            if (nxt <= r[j]) kfirst += __ldg(S + (uint64_t)j * top + (r[j] - nxt));
+        }
+        while (left > 0) {
+            const uint64_t rk = sel_u64(r, k);
+            const uint64_t gk = G.g[k];
+            const uint32_t v = sel_u32(a, k);
+            const int32_t vv = (int32_t)v - lane;
+            const bool valid = vv >= 0;
+            const uint64_t p = valid ? rk - (uint64_t)vv * gk : 0;
+            // child leaf type and rows
+            uint64_t cnt = 0, mrow = 0;
+            bool leaf = false;
+            if (k + 3 == D) {   // PROG
+                uint32_t w0 = 0, l0 = 0;
+                cnt = valid ? prog_block(P, (uint32_t)p, w0, l0) : 0;
+                if (lane == 0 && kfirst) {
+                    w0 -= (uint32_t)kfirst * P.h1;
+                    l0 += (uint32_t)kfirst * P.g1;
+                }
+                mrow = kComputed | kProg | ((uint64_t)l0 << 30) | w0;
+                leaf = true;
+            } else if (k + 2 == D) {   // DIRECT
+                cnt = (valid && p % hl == 0) ? 1 : 0;
+                mrow = kComputed | ((p / hl) << 30);
+                leaf = true;
+            } else {
+                cnt = valid ? __ldg(S + (uint64_t)(k + 1) * top + p) : 0;
+                leaf = (k + 1 >= L) && p < ltop;
+                if (leaf && cnt) mrow = __ldg(off + p + 1) - cnt + (lane == 0 ? kfirst : 0);
+            }
+            const unsigned dball = __ballot_sync(kFull, !leaf && cnt > 0);
+            const int dl = dball ? __ffs(dball) - 1 : 32;
+            uint32_t c = (leaf && lane < dl) ? (uint32_t)cnt : 0u;
+            if (lane == 0) c -= (uint32_t)kfirst;
+            kfirst = 0;
+            uint32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t u = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += u;
+            }
+            const uint32_t excl = incl - c;
+            const uint32_t total = __shfl_sync(kFull, incl, 31);
+            const uint32_t use = (uint64_t)total < left ? total : (uint32_t)left;
+            const uint32_t cc = excl >= use ? 0u : (c < use - excl ? c : use - excl);
+            const unsigned nz = __ballot_sync(kFull, cc > 0);
+            if (cc > 0) {
+                const int e = __popc(nz & ((1u << lane) - 1));
+                bi[e].memo_row = mrow;
+                bi[e].start = excl;
+                bi[e].v = (uint32_t)vv;
+            }
+            __syncwarp();
+            int e0 = 0;
+            for (uint32_t q0 = 0; q0 < use; q0 += 32) {
+                const unsigned bit = (cc > 0 && excl >= q0 && excl - q0 < 32) ? (1u << (excl - q0)) : 0u;
+                const unsigned M = __reduce_or_sync(kFull, bit);
+                if (q0 != 0) e0 += (int)(M & 1u);
+                const uint32_t q = q0 + lane;
+                const int e = e0 + __popc(M & ((2u << lane) - 2u));
+                e0 += __popc(M & 0xfffffffeu);
+                if (q < use) {
+                    const BlockInfo info = bi[e];
+                    const uint32_t jq = q - info.start;
+                    const uint64_t mr = info.memo_row;
+                    uint32_t tw[T];
+#pragma unroll
+                    for (int j = 0; j < T; ++j) tw[j] = 0;
+                    uint32_t c2 = 0, c1 = 0;   // computed a_{d-2}, a_{d-1}
+                    if (mr & kComputed) {
+                        c2 = (uint32_t)(mr & 0x3fffffffu) - jq * P.h1;
+                        c1 = (uint32_t)((mr >> 30) & 0x3fffffffu) + jq * P.g1;
+                    } else {
+                        load_tail<T>(memo + (mr + jq) * T, tw);
+                    }
+                    uint32_t wv[D];
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        // j < k: the walk's prefix; j == k: the child; j > k: the leaf's rows
+                        uint32_t x = (j >= L) ? tw[j >= L ? j - L : 0] : 0u;
+                        if (mr & kComputed) {
+                            if (j == D - 2) x = c2;
+                            if (j == D - 1) x = c1;
+                        }
+                        if (j < k) x = a[j];
+                        if (j == k) x = info.v;
+                        wv[j] = x;
+                    }
+                    if constexpr (MODE == FZ_MATERIALIZE) {
+                        store_row<D>(out + (outpos + q) * (uint64_t)D, wv);
+                    } else {
+                        acc_hash += row_hash<D>(row_base + outpos + q, wv);
+                    }
+                }
+            }
+            __syncwarp();
+            acc_rows += (lane == 0) ? use : 0;
+            outpos += use;
+            left -= use;
+            if (left == 0) break;
+            if (dl < 32) {   // descend into child v - dl
+                const uint32_t av = v - (uint32_t)dl;
+                const uint64_t rn = rk - (uint64_t)av * gk;
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    if (j == k) a[j] = av;
+                    if (j == k + 1) a[j] = (uint32_t)(rn / G.g[j]);
+                    if (j == k + 1) r[j] = rn;
+                }
+                ++k;
+                continue;
+            }
+            // rows left under the current prefix with a_k <= w: S_k[r_k] - S_k[r_k - (w + 1) g_k]
+            auto rows_left = [&](int kk, uint32_t w) {
+                const uint64_t rr = sel_u64(r, kk), nx = ((uint64_t)w + 1) * G.g[kk];
+                const uint64_t *Sk = S + (uint64_t)kk * top;
+                return __ldg(Sk + rr) > (nx <= rr ? __ldg(Sk + (rr - nx)) : 0ull);
+            };
+            if (v >= 32 && rows_left(k, v - 32)) {   // next 32 siblings
+#pragma unroll
+                for (int j = 0; j < D; ++j)
+                    if (j == k) a[j] = v - 32;
+                continue;
+            }
+            // no rows among the remaining children: back up to the nearest ancestor with a next sibling
+            // that still has rows (nextCandidate)
+            bool more = false;
+            while (k > 0) {
+                --k;
+                const uint32_t ak = sel_u32(a, k);
+                if (ak > 0 && rows_left(k, ak - 1)) {
+#pragma unroll
+                    for (int j = 0; j < D; ++j)
+                        if (j == k) a[j] = ak - 1;
+                    more = true;
+                    break;
+                }
+            }
+            if (!more) break;   // end of stream
+        }
+    }
+    acc_rows = warp_sum_u64(acc_rows);
+    if (lane == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)acc_rows);
+    if constexpr (MODE == FZ_HASH) {
+        acc_hash = warp_sum_u64(acc_hash);
+        if (lane == 0) atomicAdd((unsigned long long *)(hdr->result + 1), (unsigned long long)acc_hash);
     }
 }
 

@@ -30,7 +30,10 @@ class FzError(RuntimeError):
 class _MemoInfo(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int), ("t", ctypes.c_int), ("top", ctypes.c_uint64), ("entries", ctypes.c_uint64),
                 ("max_card", ctypes.c_uint64), ("batches", ctypes.c_uint64), ("batch", ctypes.c_uint32),
-                ("fill_mode", ctypes.c_int), ("window_rows", ctypes.c_uint64)]
+                ("fill_mode", ctypes.c_int), ("window_rows", ctypes.c_uint64), ("memo_top", ctypes.c_uint64)]
+
+MEMO_TOP_AUTO = 0                 # fz_layout_create_partial: largest memo_top whose rows fit the cap
+MEMO_TOP_FULL = (1 << 64) - 1     # memo_top = top
 
 
 def _load():
@@ -50,6 +53,7 @@ def _load():
         "fz_plan_create": [vp, u64, c_int, c_int, c_int, vp, u64, vp, ctypes.POINTER(vp)],
         "fz_plan_shard": [vp, vp, u64p, u64p, u64p],
         "fz_layout_create": [u32p, c_int, c_int, u64, c_int, ctypes.POINTER(vp)],
+        "fz_layout_create_partial": [u32p, c_int, c_int, u64, u64, c_int, ctypes.POINTER(vp)],
         "fz_layout_workspace_bytes": [vp, u64p],
         "fz_layout_get_info": [vp, ctypes.POINTER(_MemoInfo)],
         "fz_memo_build_layout": [vp, vp, u64, vp, ctypes.POINTER(vp)],
@@ -128,13 +132,19 @@ def set_fill_mode(mode: int) -> None:
 
 
 class Layout:
-    """A1 host object (fz_layout): validation, sizing and host tables for (gens, t, top)."""
+    """A1 host object (fz_layout): validation, sizing and host tables for (gens, t, top).
+    memo_top (partial memo, fz_layout_create_partial): memo rows only for x < memo_top; None = full,
+    MEMO_TOP_AUTO = the largest that fits the memo cap."""
 
-    def __init__(self, gens, t: int, top: int, entries: bool = True):
+    def __init__(self, gens, t: int, top: int, entries: bool = True, memo_top: int | None = None):
         self.gens = tuple(int(g) for g in gens)
         self.d, self.t, self.top, self.entries = len(self.gens), int(t), int(top), bool(entries)
         h = ctypes.c_void_p()
-        _check(_L.fz_layout_create(_gens(self.gens), self.d, self.t, self.top, int(entries), ctypes.byref(h)))
+        if memo_top is None:
+            _check(_L.fz_layout_create(_gens(self.gens), self.d, self.t, self.top, int(entries), ctypes.byref(h)))
+        else:
+            _check(_L.fz_layout_create_partial(_gens(self.gens), self.d, self.t, self.top, int(memo_top),
+                                               int(entries), ctypes.byref(h)))
         self.h = h
         nbytes = ctypes.c_uint64()
         _check(_L.fz_layout_workspace_bytes(self.h, ctypes.byref(nbytes)))
@@ -200,8 +210,10 @@ class Memo:
         return rows, off, S
 
 
-def memo_build(gens, t: int, top: int, *, entries: bool = True, device=None, stream=None) -> Memo:
-    return Memo(gens, t, top, entries=entries, device=device, stream=stream)
+def memo_build(gens, t: int, top: int, *, entries: bool = True, device=None, stream=None,
+               memo_top: int | None = None) -> Memo:
+    lay = Layout(gens, t, top, entries, memo_top=memo_top)
+    return Memo(layout=lay, device=device, stream=stream)
 
 
 def count(memo: Memo, n: int, stream=None) -> int:

@@ -86,3 +86,36 @@ def test_recommend_t():
     assert t == 3 and 4 not in cost and cost[3] < cost[2]
     t, cost = fz.recommend_t((97, 98, 99, 100, 101, 102, 103, 104), 10000, "count")
     assert cost[3] < cost[2] < cost[1]
+
+
+def test_partial_layout(corc):
+    """f2 sizing (fz_layout_create_partial): rows only for x < memo_top, AUTO = the largest memo_top
+    whose rows fit the cap, memo_top > top rejected.  Host only."""
+    from paper_2407_20474_b200 import fz
+
+    g, n, t = (11, 13, 17, 19), 30232, 2
+    card = corc.gf_table(n, g[2:])
+    full = fz.Layout(g, t, n + 1)
+    assert full.info["memo_top"] == n + 1 and full.info["entries"] == int(card.sum()) == 1_416_553
+    lay = fz.Layout(g, t, n + 1, memo_top=10000)
+    assert lay.info["memo_top"] == 10000 and lay.info["top"] == n + 1
+    assert lay.info["entries"] == int(card[:10000].sum())
+    assert lay.workspace_bytes < full.workspace_bytes
+    assert fz.Layout(g, t, n + 1, memo_top=fz.MEMO_TOP_FULL).info["memo_top"] == n + 1
+    cap = 4 * t * 700_000
+    fz.set_memo_cap(cap)
+    try:
+        auto = fz.Layout(g, t, n + 1, memo_top=fz.MEMO_TOP_AUTO)
+        mt = auto.info["memo_top"]
+        assert int(card[:mt].sum()) * 4 * t <= cap < int(card[:mt + 1].sum()) * 4 * t
+        with pytest.raises(fz.FzError) as e:
+            fz.Layout(g, t, n + 1)                            # the full memo is above the cap
+        assert e.value.status == 3
+    finally:
+        fz.set_memo_cap(0)
+    with pytest.raises(fz.FzError) as e:
+        fz.Layout(g, t, n + 1, memo_top=n + 2)
+    assert e.value.status == 1
+    # t = 0 and count-only layouts have no rows: memo_top is top
+    assert fz.Layout(g, 0, n + 1, memo_top=5).info["memo_top"] == n + 1
+    assert fz.Layout(g, t, n + 1, entries=False, memo_top=5).info["memo_top"] == n + 1

@@ -290,3 +290,93 @@ def test_device_plan_matches_host_cut(mode):
         for s in range(ns):
             p = fz.Plan(memo, n, mode, s, ns)
             assert (p.row_begin, p.rows) == (rb[s], rl[s]), (mode, ns, s)
+
+
+# --------------------------------------------- f2: partial memo (topOfMemo <= n)
+@pytest.mark.parametrize("seed", range(60))
+def test_partial_random(seed, corc):
+    """memo rows only for x < memo_top <= n.  Every t in 1..d and
+    several memo_top: the list == O1 and == Alg 5 run with the same topOfMemo (the paper's Else
+    branch), hash and count bit-exact, shard invariance over 1 and 3 shards."""
+    g, n, _ = random_instance(seed)
+    want, cnt, h = corc.enumerate(n, g)
+    for t in range(1, len(g) + 1):
+        for mt in sorted({1, max(1, n // 3), max(1, n // 2 + 1), max(1, n)}):
+            memo = fz.memo_build(g, t, n + 1, memo_top=mt)
+            assert memo.info["memo_top"] == mt
+            parts, hs = [], 0
+            for ns in (1, 3):
+                parts, hs = [], 0
+                for s in range(ns):
+                    out, r, _ = fz.enumerate(memo, n, "materialize", shard=s, nshards=ns)
+                    parts.append(_np(out).reshape(-1, len(g))[:r])
+                    hs = (hs + fz.enumerate(memo, n, "hash", shard=s, nshards=ns)[2]) % (1 << 64)
+                got = np.concatenate(parts)
+                assert np.array_equal(got, want.reshape(-1, len(g))), (t, mt, ns)
+                assert hs == h, (t, mt, ns)
+            assert fz.enumerate(memo, n, "count")[1] == cnt
+            if t < len(g) and n <= 80 and seed % 4 == 0:
+                alg5 = np.array(O.alg5_run(n, g, t, top=mt), dtype=np.uint32).reshape(-1, len(g))
+                assert np.array_equal(got, alg5), (t, mt)
+
+
+@pytest.mark.parametrize("tail,top,mt", [((9, 20), 1001, 400), ((17, 19), 30233, 9000), ((3, 5, 8), 500, 137),
+                                         ((38, 40, 41, 42), 3001, 1500)], ids=lambda x: str(x))
+def test_partial_memo_rows(tail, top, mt, corc):
+    """The partial memo holds exactly Alg 2's F[0..memo_top-1] (CSR) while the count tables cover
+    every x < top."""
+    g = (5,) + tuple(tail)
+    memo = fz.memo_build(g, len(tail), top, memo_top=mt)
+    rows, off, S = memo.views()
+    want_rows, want_off = corc.memo_alg2(tail, mt)
+    assert memo.info["entries"] == len(want_rows)
+    assert np.array_equal(_np(rows).reshape(-1, len(tail)), want_rows)
+    assert np.array_equal(off.cpu().numpy().astype(np.uint64)[:mt + 1], want_off)
+    Sh = S.cpu().numpy().astype(np.uint64)
+    for i in range(len(g)):
+        assert np.array_equal(Sh[i], corc.gf_table(top - 1, g[i:])), i
+
+
+@pytest.mark.parametrize("frac", [0.5, 0.9])
+def test_partial_c2(frac, corc):
+    """C2 with a partial memo (memo_top = frac * n), in bench.py's launch configuration: 100 000 681
+    rows element by element against O2, hash == SURVEY App. A."""
+    g, n, t = C2.gens, C2.n, C2.t
+    memo = fz.memo_build(g, t, n + 1, memo_top=int(frac * n))
+    out, rows, _ = fz.enumerate(memo, n, "materialize")
+    want, cnt, h = corc.enumerate(n, g, use_o2=True)
+    assert rows == cnt == 100_000_681
+    assert np.array_equal(_np(out).reshape(-1, 4), want)
+    assert fz.enumerate(memo, n, "hash")[1:] == (cnt, 0x5FC4E1F53888C565)
+
+
+def test_partial_auto_cap(corc):
+    """memo_top = AUTO under a small cap: the largest memo_top whose rows fit, and the same rows."""
+    g, n = (13, 37, 38, 40, 41), 3000
+    full = fz.memo_build(g, 3, n + 1)
+    cap = full.info["entries"] * 4 * 3 // 5
+    fz.set_memo_cap(cap)
+    try:
+        memo = fz.memo_build(g, 3, n + 1, memo_top=fz.MEMO_TOP_AUTO)
+        mt = memo.info["memo_top"]
+        assert 1 <= mt <= n
+        card = corc.gf_table(n, g[2:])
+        assert memo.info["entries"] == int(card[:mt].sum()) and memo.info["entries"] * 12 <= cap
+        assert (int(card[:mt + 1].sum())) * 12 > cap
+        want, cnt, h = corc.enumerate(n, g)
+        out, rows, _ = fz.enumerate(memo, n, "materialize")
+        assert rows == cnt and np.array_equal(_np(out).reshape(-1, 5)[:rows], want)
+        # the end-to-end host call goes partial instead of failing with FZ_ECAP
+        assert fz.run_host(g, 3, n, "hash") == (cnt, h)
+    finally:
+        fz.set_memo_cap(0)
+
+
+@pytest.mark.parametrize("d,md,n", [r for r in TABLE1_ROWS if r[2] <= 3000][:8], ids=lambda x: str(x))
+def test_partial_table1(d, md, n, corc):
+    """Table 1 generators with a memo to n/2 only: hash and count == oracle."""
+    g = table1_gens(d)
+    memo = fz.memo_build(g, md, n + 1, memo_top=n // 2 + 1)
+    cnt, h = corc.count_hash(n, g, use_o2=True)
+    assert fz.enumerate(memo, n, "hash")[1:] == (cnt, h)
+    assert fz.enumerate(memo, n, "count")[1] == cnt

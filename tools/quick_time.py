@@ -20,6 +20,11 @@ CFG = {
     "C4": ((97, 98, 99, 100, 101, 102, 103, 104), 40000, 3, "count"),
     "T1": ((13, 37, 38, 40, 41, 42, 43, 44), 2000, 4, "materialize"),
 }
+# partial memo (f2): memo rows only for x < frac * n
+for _f in (10, 25, 50, 75, 90):
+    CFG[f"C2p{_f}"] = CFG["C2"] + (_f,)
+    CFG[f"C2hp{_f}"] = CFG["C2h"] + (_f,)
+CFG["C3t3p50"] = CFG["C3t3"] + (50,)
 
 
 def ev():
@@ -32,8 +37,9 @@ def main():
     fz.set_memo_cap(64 << 30)   # C3 t=4: 30.4 GB memo (above the 8e9 default)
     names = sys.argv[1:] or ["C2"]
     for name in names:
-        g, n, t, mode = CFG[name]
-        lay = fz.Layout(g, t, n + 1, entries=(mode != "count"))
+        g, n, t, mode, *pct = CFG[name]
+        mt = n * pct[0] // 100 if pct else None
+        lay = fz.Layout(g, t, n + 1, entries=(mode != "count"), memo_top=mt)
         ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device="cuda")
         memo = fz.Memo(layout=lay, workspace=ws)
         pws = torch.empty(fz.plan_workspace_bytes(memo), dtype=torch.uint8, device="cuda")
