@@ -533,7 +533,8 @@ fz_status launch_deep_dt(int mode, const WalkArgs &a, const uint64_t *S, uint64_
     static thread_local int per_sm[2] = {0, 0};
     int &ps = per_sm[mode == FZ_MATERIALIZE ? 0 : 1];
     if (!ps) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, fzk::kWalkThreads, 0) != cudaSuccess || ps < 1)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, fzk::kWalkThreads, 4096 * 8) != cudaSuccess ||
+            ps < 1)
             ps = 2;
         ps = std::min(ps, 8);
     }
@@ -556,8 +557,10 @@ fz_status launch_deep_dt(int mode, const WalkArgs &a, const uint64_t *S, uint64_
         }
         P.inv = P.h1 == 1 ? 0u : (uint32_t)(((s0 % (int64_t)P.h1) + P.h1) % P.h1);
     }
-    kern<<<(unsigned)(device_sms() * ps), fzk::kWalkThreads, 0, s>>>(a.G, a.n, a.hdr, S, a.top, ltop, off, a.wt.memo,
-                                                                      a.out, a.cap, a.row_base, P);
+    const uint64_t f0 = a.n / a.G.g[0] + 1;
+    const uint32_t f0n = (f0 <= 4096) ? (uint32_t)f0 : 0u;
+    kern<<<(unsigned)(device_sms() * ps), fzk::kWalkThreads, (size_t)f0n * 8, s>>>(
+        a.G, a.n, a.hdr, S, a.top, ltop, off, a.wt.memo, a.out, a.cap, a.row_base, P, f0n);
     ++g_launches;
     return cuda_check("k5_deep");
 }

@@ -1462,10 +1462,14 @@ __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, Pl
                                                         const uint64_t *__restrict__ S, uint64_t top, uint64_t ltop,
                                                         const uint64_t *__restrict__ off,
                                                         const uint32_t *__restrict__ memo, uint32_t *out,
-                                                        uint64_t out_cap_rows, uint64_t row_base, ProgGens P)
+                                                        uint64_t out_cap_rows, uint64_t row_base, ProgGens P,
+                                                        uint32_t f0n)
 {
     constexpr int L = D - T;
     static_assert(T >= 1 && MODE != FZ_COUNT, "partial walk: rows of a memo with t >= 1");
+    extern __shared__ uint64_t f0s[];   // level-0 unrank column S_0[n - q g_0] (f0n entries, 0 = not cached)
+    for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(S + (n64 - (uint64_t)q * G.g[0]));
+    if (f0n) __syncthreads();
     __shared__ BlockInfo binfo[kWalkThreads / 32][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t nslices = hdr->nslices, slice_len = hdr->slice_len, shard_begin = hdr->shard_begin,
@@ -1486,28 +1490,39 @@ __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, Pl
         const uint64_t begin = s * slice_len;
         uint64_t left = (shard_len - begin) < slice_len ? (shard_len - begin) : slice_len;
         uint64_t outpos = begin;
-        // the slice's first row, all d coordinates (the S tables cover every x <= n)
+        // unrank the slice's first row level by level (the S tables cover every x <= n) down to the
+        // leaf that holds it (same rules as the walk below); kfirst = its offset inside that leaf
         uint32_t a[D];
         uint64_t r[D + 1];
-        {
-            uint32_t ua[kMaxD];
-            unrank(S, top, G, D, n64, shard_begin + begin, ua);
-#pragma unroll
-            for (int j = 0; j < D; ++j) a[j] = ua[j];
-        }
+        int k = 0;
+        uint64_t kfirst = shard_begin + begin;
         r[0] = n64;
 #pragma unroll
-        for (int j = 0; j < D; ++j) r[j + 1] = r[j] - (uint64_t)a[j] * G.g[j];
-        // the leaf holding this row (same rules as the walk below)
-        int k = 0;
-        while (!(k + 3 == D || k + 2 == D || (k + 1 >= L && sel_u64(r, k + 1) < ltop))) ++k;
-        // offset of the row inside its leaf: its rank over coordinates k+1..d-1
-        uint64_t kfirst = 0;
+        for (int j = 0; j < D; ++j) {
+            a[j] = 0;
+            r[j + 1] = 0;
+        }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            if (j <= k) continue;
-            const uint64_t nxt = ((uint64_t)a[j] + 1) * G.g[j];
-            if (nxt <= r[j]) kfirst += __ldg(S + (uint64_t)j * top + (r[j] - nxt));
+            if (j > k) continue;
+            const uint64_t rj = r[j], gj = G.g[j], amax = rj / gj;
+            const uint64_t *Tj = S + (uint64_t)j * top;
+            const bool cached = (j == 0) && f0n != 0;
+            uint64_t lo = 0, hi = amax;   // a_j = max{a : S_j[r_j - a g_j] > kfirst}
+            while (lo < hi) {
+                const uint64_t step = (hi - lo + 31) / 32;
+                const uint64_t cand = lo + (uint64_t)(lane + 1) * step;
+                const bool pred = cand <= hi && (cached ? f0s[cand] : __ldg(Tj + (rj - cand * gj))) > kfirst;
+                const int m = __popc(__ballot_sync(kFull, pred));
+                const uint64_t nlo = lo + (uint64_t)m * step;
+                uint64_t nhi = lo + (uint64_t)(m + 1) * step - 1;
+                hi = nhi > hi ? hi : nhi;
+                lo = nlo;
+            }
+            a[j] = (uint32_t)lo;
+            if (lo + 1 <= amax) kfirst -= cached ? f0s[lo + 1] : __ldg(Tj + (rj - (lo + 1) * gj));
+            r[j + 1] = rj - lo * gj;
+            if (!(j + 3 == D || j + 2 == D || (j + 1 >= L && r[j + 1] < ltop))) ++k;
         }
         while (left > 0) {
             const uint64_t rk = sel_u64(r, k);
@@ -1560,45 +1575,57 @@ __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, Pl
                 bi[e].v = (uint32_t)vv;
             }
             __syncwarp();
+            constexpr int UNR = 1;   // (UNR = 4 measured slower here: the computed rows need no loads)
             int e0 = 0;
-            for (uint32_t q0 = 0; q0 < use; q0 += 32) {
-                const unsigned bit = (cc > 0 && excl >= q0 && excl - q0 < 32) ? (1u << (excl - q0)) : 0u;
-                const unsigned M = __reduce_or_sync(kFull, bit);
-                if (q0 != 0) e0 += (int)(M & 1u);
-                const uint32_t q = q0 + lane;
-                const int e = e0 + __popc(M & ((2u << lane) - 2u));
-                e0 += __popc(M & 0xfffffffeu);
-                if (q < use) {
-                    const BlockInfo info = bi[e];
-                    const uint32_t jq = q - info.start;
-                    const uint64_t mr = info.memo_row;
-                    uint32_t tw[T];
+            for (uint32_t q0 = 0; q0 < use; q0 += 32 * UNR) {
+                uint32_t wv[UNR][D];
+                bool ok[UNR];
 #pragma unroll
-                    for (int j = 0; j < T; ++j) tw[j] = 0;
-                    uint32_t c2 = 0, c1 = 0;   // computed a_{d-2}, a_{d-1}
-                    if (mr & kComputed) {
-                        c2 = (uint32_t)(mr & 0x3fffffffu) - jq * P.h1;
-                        c1 = (uint32_t)((mr >> 30) & 0x3fffffffu) + jq * P.g1;
-                    } else {
-                        load_tail<T>(memo + (mr + jq) * T, tw);
-                    }
-                    uint32_t wv[D];
+                for (int u = 0; u < UNR; ++u) {
+                    const uint32_t qb = q0 + 32 * u;
+                    const unsigned bit = (cc > 0 && excl >= qb && excl - qb < 32) ? (1u << (excl - qb)) : 0u;
+                    const unsigned M = __reduce_or_sync(kFull, bit);
+                    if (qb != 0) e0 += (int)(M & 1u);
+                    const uint32_t q = qb + lane;
+                    const int e = e0 + __popc(M & ((2u << lane) - 2u));
+                    e0 += __popc(M & 0xfffffffeu);
+                    ok[u] = q < use;
+                    if (ok[u]) {
+                        const BlockInfo info = bi[e];
+                        const uint32_t jq = q - info.start;
+                        const uint64_t mr = info.memo_row;
+                        uint32_t tw[T];
 #pragma unroll
-                    for (int j = 0; j < D; ++j) {
-                        // j < k: the walk's prefix; j == k: the child; j > k: the leaf's rows
-                        uint32_t x = (j >= L) ? tw[j >= L ? j - L : 0] : 0u;
+                        for (int j = 0; j < T; ++j) tw[j] = 0;
+                        uint32_t c2 = 0, c1 = 0;   // computed a_{d-2}, a_{d-1}
                         if (mr & kComputed) {
-                            if (j == D - 2) x = c2;
-                            if (j == D - 1) x = c1;
+                            c2 = (uint32_t)(mr & 0x3fffffffu) - jq * P.h1;
+                            c1 = (uint32_t)((mr >> 30) & 0x3fffffffu) + jq * P.g1;
+                        } else {
+                            load_tail<T>(memo + (mr + jq) * T, tw);
                         }
-                        if (j < k) x = a[j];
-                        if (j == k) x = info.v;
-                        wv[j] = x;
+#pragma unroll
+                        for (int j = 0; j < D; ++j) {
+                            // j < k: the walk's prefix; j == k: the child; j > k: the leaf's rows
+                            uint32_t x = (j >= L) ? tw[j >= L ? j - L : 0] : 0u;
+                            if (mr & kComputed) {
+                                if (j == D - 2) x = c2;
+                                if (j == D - 1) x = c1;
+                            }
+                            if (j < k) x = a[j];
+                            if (j == k) x = info.v;
+                            wv[u][j] = x;
+                        }
                     }
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    if (!ok[u]) continue;
+                    const uint32_t q = q0 + 32 * u + lane;
                     if constexpr (MODE == FZ_MATERIALIZE) {
-                        store_row<D>(out + (outpos + q) * (uint64_t)D, wv);
+                        store_row<D>(out + (outpos + q) * (uint64_t)D, wv[u]);
                     } else {
-                        acc_hash += row_hash<D>(row_base + outpos + q, wv);
+                        acc_hash += row_hash<D>(row_base + outpos + q, wv[u]);
                     }
                 }
             }
@@ -1625,7 +1652,7 @@ __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, Pl
                 const uint64_t *Sk = S + (uint64_t)kk * top;
                 return __ldg(Sk + rr) > (nx <= rr ? __ldg(Sk + (rr - nx)) : 0ull);
             };
-            if (v >= 32 && rows_left(k, v - 32)) {   // next 32 siblings
+            if (v >= 32 && (k + 3 >= D || rows_left(k, v - 32))) {   // next 32 siblings (PROG: no test)
 #pragma unroll
                 for (int j = 0; j < D; ++j)
                     if (j == k) a[j] = v - 32;
