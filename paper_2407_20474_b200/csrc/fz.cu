@@ -118,6 +118,7 @@ struct Sizing {
     int d, t, L;
     uint64_t top;
     uint64_t ltop = 0;   // memo rows cover x < ltop <= top (topOfMemo); tables cover x < top
+    uint64_t card_max_all = 0;   // max_x<top |Z(x; tail)| (the COUNT walk reads card up to n)
     uint64_t entries = 0, max_card = 0, window = 0, ring_rows = 0, batches = 0;
     uint32_t batch = 0;
     uint32_t stage_words = 0;   // fill mode 1: words per TMA link chunk buffer
@@ -169,6 +170,7 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
         return fail(FZ_EINVAL, "memo_top=%llu > top=%llu", (unsigned long long)memo_top, (unsigned long long)top);
     }
     z.ltop = memo_top;
+    for (uint64_t x = 0; x < top; ++x) z.card_max_all = std::max(z.card_max_all, card[x]);
     const uint64_t ltop = memo_top;
     uint64_t entries = 0, mx = 0;
     for (uint64_t x = 0; x < ltop; ++x) {
@@ -444,7 +446,11 @@ fz_status launch_fill(const fz_memo *m, cudaStream_t s)
     }
 }
 
+constexpr uint64_t kCountSmemMax = 100 * 1024;   // COUNT u16 card table in shared memory (2 CTAs / SM)
+
 struct WalkArgs {
+    uint64_t card_max = ~0ull;   // max card over every x < top (COUNT smem staging needs < 2^16)
+    uint64_t prefixes = 0;       // leading prefixes of the whole walk (W_0[n])
     Gens G;
     uint64_t n;
     PlanHdr *hdr;
@@ -459,21 +465,38 @@ struct WalkArgs {
 template <int D, int T, int MODE>
 fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
 {
-    // persistent grid: exactly the resident CTAs (the walk is a grid-stride loop over slices)
-    static thread_local int per_sm = 0;
-    if (!per_sm) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::kWalkThreads,
-                                                          4096 * 8) !=
-                cudaSuccess ||
-            per_sm < 1)
-            per_sm = 4;
-        per_sm = std::min(per_sm, 8);
-    }
     // level-0 unrank column in shared memory when it is short (<= 4096 entries, 32 KB)
     const uint64_t f0 = a.n / a.G.g[0] + 1;
     const uint32_t f0n = (f0 <= 4096) ? (uint32_t)f0 : 0u;
-    fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::kWalkThreads, (size_t)f0n * 8, s>>>(
-        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n);
+    // COUNT: the residue-major card table as u16 in shared memory when its values and size allow
+    static const bool c16_env = [] {
+        const char *e = getenv("FZ_COUNT_SMEM");
+        return !(e && e[0] == '0');
+    }();
+    // (n + 1 entries, when the walk has enough prefixes per CTA to repay the staging)
+    const uint64_t cn = a.n + 1;
+    const uint32_t c16n = (MODE == FZ_COUNT && D - T >= 2 && c16_env && a.card_max < 65536 &&
+                           a.card_max * (a.n / a.wt.m + 1) < (1ull << 32) &&   // per-lane u32 run sums
+                           cn * 2 + f0n * 8 <= kCountSmemMax && a.prefixes >= cn * 64 * (uint64_t)device_sms())
+                              ? (uint32_t)cn
+                              : 0u;
+    const size_t smem = (size_t)f0n * 8 + ((size_t)c16n * 2 + 7) / 8 * 8;
+    // persistent grid: exactly the resident CTAs (the walk is a grid-stride loop over slices)
+    static thread_local size_t last_smem = ~(size_t)0;
+    static thread_local int per_sm = 0;
+    if (smem != last_smem) {
+        if (smem > 48 * 1024)
+            FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::kWalkThreads,
+                                                          std::max<size_t>(smem, 4096 * 8)) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        per_sm = std::min(per_sm, 8);
+        last_smem = smem;
+    }
+    fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::kWalkThreads, smem, s>>>(
+        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n, c16n);
     ++g_launches;
     return cuda_check("k5_walk");
 }
@@ -1016,6 +1039,10 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
     a.wt.memo = m->rows;
     const uint64_t gl = z.L > 0 ? m->lay->g[z.L - 1] : 1;
     a.wt.R = (z.top + gl - 1) / gl;
+    a.wt.m = (uint32_t)gl;
+    a.wt.card64 = m->S + (uint64_t)z.L * z.top;
+    a.card_max = z.card_max_all;
+    a.prefixes = m->lay->H.W.empty() ? 0 : m->lay->H.W[p->n];
     a.out = d_out;
     a.cap = (p->mode == FZ_MATERIALIZE) ? out_capacity_rows : ~0ull;
     a.row_base = row_base;

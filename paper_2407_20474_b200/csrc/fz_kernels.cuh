@@ -1172,6 +1172,8 @@ struct WalkTables {
     const uint32_t *cardT;   // residue-major card (w.r.t. m = g_L)
     const uint64_t *offT;    // residue-major CSR offsets
     const uint32_t *memo;    // CSR rows, t u32 each
+    const uint64_t *card64;  // card = S_L, natural layout
+    uint32_t m;              // g_L (residue modulus of cardT / offT)
     uint64_t R;              // rows per residue column
 };
 
@@ -1179,11 +1181,14 @@ template <int D, int T, int MODE>
 __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
-                                                         uint32_t f0n)
+                                                         uint32_t f0n, uint32_t c16n)
 {
     extern __shared__ uint64_t f0s[];   // level-0 unrank column (f0n entries, 0 = not cached)
     for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Tb + (n64 - (uint64_t)q * G.g[0]));
-    if (f0n) __syncthreads();
+    // COUNT: card[x] = S_L[x], x < c16n, as u16 in shared memory after f0s (natural layout; 0 = not staged)
+    uint16_t *c16 = reinterpret_cast<uint16_t *>(f0s + f0n);
+    for (uint32_t q = threadIdx.x; q < c16n; q += blockDim.x) c16[q] = (uint16_t)__ldg(wt.card64 + q);
+    if (f0n || c16n) __syncthreads();
     constexpr int L = D - T;
     static_assert(L >= 1, "at least one leading coordinate");
     __shared__ BlockInfo binfo[kWalkThreads / 32][32];
@@ -1237,28 +1242,19 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
         uint64_t left = sl.len;
         uint64_t outpos = sl.begin;
         if constexpr (MODE == FZ_COUNT) {
-            // COUNT walk: every leading prefix adds card[p], p = n - phi(prefix).  The innermost run
-            // v, v-1, .., 0 is the contiguous residue-major segment [col R + q - v, col R + q]; the
-            // common carry (a_{L-1} > 0) moves r_in by g_{L-1} without a division.
+            // COUNT walk: every leading prefix adds card[p], p = n - phi(prefix) (one card lookup per
+            // leading prefix).  An innermost run v, v-1, .., 0 is the contiguous residue-major segment
+            // [col R + q - v, col R + q]: a run is summed by the 32 lanes together (the slice's partial
+            // first and last runs, and every run when the card table is not staged).  With the card
+            // table staged in shared memory (u16, natural layout), whole runs go one per lane: lane l
+            // takes sibling a_{L-2} - l and sums card[r_l - v m], v = 0..r_l / m, so the per-run
+            // bookkeeping is shared by 32 runs.
             uint32_t q = r_in / m, col = r_in - q * m;
             uint32_t vv = (uint32_t)v;
             uint32_t left32 = (uint32_t)left;   // K4 keeps COUNT slices below 2^31 prefixes
-            for (;;) {
-                const uint32_t run = vv + 1;
-                const uint32_t take = left32 < run ? left32 : run;
-                const uint32_t *p = cardT + ((uint64_t)col * wt.R + (q - vv) + lane);
-                uint32_t rem = take;
-                for (; rem >= 128; rem -= 128, p += 128)
-                    acc_rows += (uint64_t)(__ldg(p) + __ldg(p + 32)) + (__ldg(p + 64) + __ldg(p + 96));
-                uint32_t part = 0;
-                if ((uint32_t)lane < rem) part += __ldg(p);
-                if ((uint32_t)lane + 32 < rem) part += __ldg(p + 32);
-                if ((uint32_t)lane + 64 < rem) part += __ldg(p + 64);
-                if ((uint32_t)lane + 96 < rem) part += __ldg(p + 96);
-                acc_rows += part;
-                left32 -= take;
-                left = left32;
-                if (left == 0 || L == 1) break;
+            const uint32_t g2 = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] : 0u;
+            // outer carry (rightmost nonzero a_i, i < L-2 ... L-1 excluded): false at end of stream
+            auto carry = [&]() -> bool {
                 if (a[L - 2] > 0) {
                     a[L - 2] -= 1;
                     col += cgr;
@@ -1272,7 +1268,7 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
 #pragma unroll
                     for (int j = 0; j < L - 1; ++j)
                         if (a[j] > 0) i = j;
-                    if (i < 0) break;   // end of stream
+                    if (i < 0) return false;
                     uint32_t r = n;
 #pragma unroll
                     for (int j = 0; j < L - 1; ++j) {
@@ -1284,7 +1280,77 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
                     col = r - q * m;
                 }
                 vv = q;
+                return true;
+            };
+            for (;;) {
+                {   // one run, warp-cooperative: v = vv .. max(0, vv + 1 - left)
+                    const uint32_t run = vv + 1;
+                    const uint32_t take = left32 < run ? left32 : run;
+                    const uint32_t *p = cardT + ((uint64_t)col * wt.R + (q - vv) + lane);
+                    uint32_t rem = take;
+                    // u64 sums: card values are unbounded in COUNT-only layouts
+                    for (; rem >= 128; rem -= 128, p += 128)
+                        acc_rows += (uint64_t)__ldg(p) + __ldg(p + 32) + __ldg(p + 64) + __ldg(p + 96);
+                    uint64_t part = 0;
+                    if ((uint32_t)lane < rem) part += __ldg(p);
+                    if ((uint32_t)lane + 32 < rem) part += __ldg(p + 32);
+                    if ((uint32_t)lane + 64 < rem) part += __ldg(p + 64);
+                    if ((uint32_t)lane + 96 < rem) part += __ldg(p + 96);
+                    acc_rows += part;
+                    left32 -= take;
+                }
+                if (left32 == 0 || L == 1 || !carry()) break;
+                if (L >= 2 && c16n) {
+                    // whole runs, one per lane, while they fit the slice's budget
+                    bool more = true;
+                    for (;;) {
+                        const uint32_t A = a[L - 2];
+                        const uint32_t rin = q * m + col;
+                        const uint32_t rl = rin + (uint32_t)lane * g2;
+                        const uint32_t len = ((uint32_t)lane <= A) ? rl / m + 1 : 0u;
+                        uint32_t incl = len;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t u = __shfl_up_sync(kFull, incl, o);
+                            if (lane >= o) incl += u;
+                        }
+                        const bool fit = len > 0 && incl <= left32;
+                        const int nf = __popc(__ballot_sync(kFull, fit));
+                        if (nf == 0) break;
+                        if (fit) {
+                            const uint16_t *cp = c16 + rl;
+                            uint32_t s0 = 0, s1 = 0;
+                            uint32_t j = 0;
+                            for (; j + 2 <= len; j += 2) {
+                                s0 += cp[-(int32_t)(j * m)];
+                                s1 += cp[-(int32_t)((j + 1) * m)];
+                            }
+                            if (j < len) s0 += cp[-(int32_t)(j * m)];
+                            acc_rows += s0 + s1;
+                        }
+                        left32 -= __shfl_sync(kFull, incl, nf - 1);
+                        if (left32 == 0) {
+                            more = false;
+                            break;
+                        }
+                        if ((uint32_t)nf <= A) {   // siblings left at level L-2: a_{L-2} = A - nf
+                            a[L - 2] = A - (uint32_t)nf;
+                            const uint32_t r2 = rin + (uint32_t)nf * g2;
+                            q = r2 / m;
+                            col = r2 - q * m;
+                            vv = q;
+                        } else {                   // level L-2 exhausted: outer carry
+                            a[L - 2] = 0;
+                            if (!carry()) {
+                                more = false;
+                                break;
+                            }
+                        }
+                    }
+                    if (!more) break;
+                }
             }
+            left = left32;
         } else {
         while (left > 0) {
             {
