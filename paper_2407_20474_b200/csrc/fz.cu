@@ -473,14 +473,19 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
         const char *e = getenv("FZ_COUNT_SMEM");
         return !(e && e[0] == '0');
     }();
-    // (n + 1 entries, when the walk has enough prefixes per CTA to repay the staging)
-    const uint64_t cn = a.n + 1;
-    const uint32_t c16n = (MODE == FZ_COUNT && D - T >= 2 && c16_env && a.card_max < 65536 &&
+    // (x <= n, residue-major with R16 entries per column: a multiple of 8 with R16 / 8 odd, so the
+    // 16-B vector loads of 8 lanes in different columns hit distinct banks), when the walk has enough
+    // prefixes per CTA to repay the staging
+    uint64_t R16 = (a.n / a.wt.m + 1 + 7) / 8 * 8;
+    if ((R16 / 8) % 2 == 0) R16 += 8;
+    const uint64_t cbytes = R16 * a.wt.m * 2;
+    const uint32_t c16R = (MODE == FZ_COUNT && D - T >= 2 && c16_env && a.card_max < 65536 &&
                            a.card_max * (a.n / a.wt.m + 1) < (1ull << 32) &&   // per-lane u32 run sums
-                           cn * 2 + f0n * 8 <= kCountSmemMax && a.prefixes >= cn * 64 * (uint64_t)device_sms())
-                              ? (uint32_t)cn
+                           cbytes + f0n * 8 + 8 <= kCountSmemMax &&
+                           a.prefixes >= (a.n + 1) * 64 * (uint64_t)device_sms())
+                              ? (uint32_t)R16
                               : 0u;
-    const size_t smem = (size_t)f0n * 8 + ((size_t)c16n * 2 + 7) / 8 * 8;
+    const size_t smem = (size_t)(f0n + 1) / 2 * 16 + (c16R ? cbytes : 0);
     // persistent grid: exactly the resident CTAs (the walk is a grid-stride loop over slices)
     static thread_local size_t last_smem = ~(size_t)0;
     static thread_local int per_sm = 0;
@@ -496,7 +501,7 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
         last_smem = smem;
     }
     fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::kWalkThreads, smem, s>>>(
-        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n, c16n);
+        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n, c16R);
     ++g_launches;
     return cuda_check("k5_walk");
 }

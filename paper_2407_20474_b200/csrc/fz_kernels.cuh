@@ -1181,14 +1181,19 @@ template <int D, int T, int MODE>
 __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
-                                                         uint32_t f0n, uint32_t c16n)
+                                                         uint32_t f0n, uint32_t c16R)
 {
     extern __shared__ uint64_t f0s[];   // level-0 unrank column (f0n entries, 0 = not cached)
     for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Tb + (n64 - (uint64_t)q * G.g[0]));
-    // COUNT: card[x] = S_L[x], x < c16n, as u16 in shared memory after f0s (natural layout; 0 = not staged)
-    uint16_t *c16 = reinterpret_cast<uint16_t *>(f0s + f0n);
-    for (uint32_t q = threadIdx.x; q < c16n; q += blockDim.x) c16[q] = (uint16_t)__ldg(wt.card64 + q);
-    if (f0n || c16n) __syncthreads();
+    // COUNT: card[x] = S_L[x], x <= n, as u16 in shared memory after f0s, residue-major w.r.t. m = g_L with
+    // c16R entries per residue column (16-B aligned columns; c16R = 0: not staged)
+    uint16_t *c16 = reinterpret_cast<uint16_t *>(f0s + ((f0n + 1) & ~1u));
+    if (c16R) {
+        const uint32_t mm = G.g[D - T - 1];
+        for (uint32_t x = threadIdx.x; x <= (uint32_t)n64; x += blockDim.x)
+            c16[(x % mm) * c16R + x / mm] = (uint16_t)__ldg(wt.card64 + x);
+    }
+    if (f0n || c16R) __syncthreads();
     constexpr int L = D - T;
     static_assert(L >= 1, "at least one leading coordinate");
     __shared__ BlockInfo binfo[kWalkThreads / 32][32];
@@ -1300,7 +1305,7 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
                     left32 -= take;
                 }
                 if (left32 == 0 || L == 1 || !carry()) break;
-                if (L >= 2 && c16n) {
+                if (L >= 2 && c16R) {
                     // whole runs, one per lane, while they fit the slice's budget
                     bool more = true;
                     for (;;) {
@@ -1317,15 +1322,32 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
                         const bool fit = len > 0 && incl <= left32;
                         const int nf = __popc(__ballot_sync(kFull, fit));
                         if (nf == 0) break;
-                        if (fit) {
-                            const uint16_t *cp = c16 + rl;
+                        if (fit) {   // entries 0..len-1 of residue column rl mod m: 16-B vectors, 2 cards per dp2a
+                            const uint32_t cl = rl - (len - 1) * m;
+                            const uint16_t *cp = c16 + cl * c16R;
+                            const uint4 *vp = reinterpret_cast<const uint4 *>(cp);
+                            const uint32_t nv = len >> 3;
                             uint32_t s0 = 0, s1 = 0;
-                            uint32_t j = 0;
-                            for (; j + 2 <= len; j += 2) {
-                                s0 += cp[-(int32_t)(j * m)];
-                                s1 += cp[-(int32_t)((j + 1) * m)];
+                            uint32_t k = 0;
+                            for (; k + 2 <= nv; k += 2) {
+                                const uint4 w0 = vp[k], w1 = vp[k + 1];
+                                s0 = __dp2a_lo(w0.x, 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.y, 0x0101u, s1);
+                                s0 = __dp2a_lo(w0.z, 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.w, 0x0101u, s1);
+                                s0 = __dp2a_lo(w1.x, 0x0101u, s0);
+                                s1 = __dp2a_lo(w1.y, 0x0101u, s1);
+                                s0 = __dp2a_lo(w1.z, 0x0101u, s0);
+                                s1 = __dp2a_lo(w1.w, 0x0101u, s1);
                             }
-                            if (j < len) s0 += cp[-(int32_t)(j * m)];
+                            if (k < nv) {
+                                const uint4 w0 = vp[k];
+                                s0 = __dp2a_lo(w0.x, 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.y, 0x0101u, s1);
+                                s0 = __dp2a_lo(w0.z, 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.w, 0x0101u, s1);
+                            }
+                            for (uint32_t j = nv * 8; j < len; ++j) s0 += cp[j];
                             acc_rows += s0 + s1;
                         }
                         left32 -= __shfl_sync(kFull, incl, nf - 1);
