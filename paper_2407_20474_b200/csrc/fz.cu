@@ -493,14 +493,14 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
         if (smem > 48 * 1024)
             FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::kWalkThreads,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::walk_threads<MODE>(),
                                                           std::max<size_t>(smem, 4096 * 8)) != cudaSuccess ||
             per_sm < 1)
             per_sm = 1;
         per_sm = std::min(per_sm, 8);
         last_smem = smem;
     }
-    fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::kWalkThreads, smem, s>>>(
+    fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::walk_threads<MODE>(), smem, s>>>(
         a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n, c16R);
     ++g_launches;
     return cuda_check("k5_walk");

@@ -1167,6 +1167,9 @@ struct BlockInfo {      // one non-empty memo block of the current warp round (1
 };
 
 constexpr int kWalkThreads = 256;
+constexpr int kCountThreads = 1024;   // COUNT walk: one CTA per SM shares one staged card table
+template <int MODE>
+constexpr int walk_threads() { return MODE == FZ_COUNT ? kCountThreads : kWalkThreads; }
 
 struct WalkTables {
     const uint32_t *cardT;   // residue-major card (w.r.t. m = g_L)
@@ -1178,7 +1181,8 @@ struct WalkTables {
 };
 
 template <int D, int T, int MODE>
-__global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
+__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : 2)))
+k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
                                                          uint32_t f0n, uint32_t c16R)
@@ -1196,8 +1200,8 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
     if (f0n || c16R) __syncthreads();
     constexpr int L = D - T;
     static_assert(L >= 1, "at least one leading coordinate");
-    __shared__ BlockInfo binfo[kWalkThreads / 32][32];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    __shared__ BlockInfo binfo[MODE == FZ_COUNT ? 1 : kWalkThreads / 32][32];   // MAT/HASH block lists
+    const int lane = threadIdx.x & 31, wib = (MODE == FZ_COUNT) ? 0 : threadIdx.x >> 5;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t n = (uint32_t)n64;
@@ -1347,7 +1351,17 @@ __global__ void __launch_bounds__(kWalkThreads, (D <= 6 ? 4 : 2)) k5_walk(Gens G
                                 s0 = __dp2a_lo(w0.z, 0x0101u, s0);
                                 s1 = __dp2a_lo(w0.w, 0x0101u, s1);
                             }
-                            for (uint32_t j = nv * 8; j < len; ++j) s0 += cp[j];
+                            const uint32_t tl = len & 7;   // last partial vector, masked
+                            if (tl) {
+                                const uint4 w0 = vp[nv];
+                                auto mk = [&](uint32_t i) {
+                                    return tl > 2 * i + 1 ? 0xffffffffu : (tl > 2 * i ? 0xffffu : 0u);
+                                };
+                                s0 = __dp2a_lo(w0.x & mk(0), 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.y & mk(1), 0x0101u, s1);
+                                s0 = __dp2a_lo(w0.z & mk(2), 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.w & mk(3), 0x0101u, s1);
+                            }
                             acc_rows += s0 + s1;
                         }
                         left32 -= __shfl_sync(kFull, incl, nf - 1);

@@ -10,8 +10,8 @@ from tools.quick_time import CFG  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-g, n, t, mode = CFG[name]
-lay = fz.Layout(g, t, n + 1, entries=(mode != "count"))
+g, n, t, mode, *pct = CFG[name]
+lay = fz.Layout(g, t, n + 1, entries=(mode != "count"), memo_top=(n * pct[0] // 100 if pct else None))
 ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device="cuda")
 memo = fz.Memo(layout=lay, workspace=ws)
 pws = torch.empty(fz.plan_workspace_bytes(memo), dtype=torch.uint8, device="cuda")
