@@ -1176,9 +1176,14 @@ struct WalkTables {
     const uint64_t *offT;    // residue-major CSR offsets
     const uint32_t *memo;    // CSR rows, t u32 each
     const uint64_t *card64;  // card = S_L, natural layout
+    uint64_t gmag[kMaxD];    // division magic of each generator: x / g_j = umulhi64(x, gmag[j]) (+x if g_j = 1)
     uint32_t m;              // g_L (residue modulus of cardT / offT)
     uint64_t R;              // rows per residue column
 };
+
+// x / g for x < 2^32 by the precomputed magic M = ceil(2^64 / g) (M = 0 encodes g = 1): the error of
+// x M / 2^64 against x / g is below x / 2^64 < 1 / g, so the floor is exact.
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint64_t M) { return M ? (uint32_t)__umul64hi(x, M) : x; }
 
 template <int D, int T, int MODE>
 __global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : 2)))
@@ -1262,6 +1267,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
             uint32_t vv = (uint32_t)v;
             uint32_t left32 = (uint32_t)left;   // K4 keeps COUNT slices below 2^31 prefixes
             const uint32_t g2 = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] : 0u;
+            const uint64_t mmag = wt.gmag[L - 1];
             // outer carry (rightmost nonzero a_i, i < L-2 ... L-1 excluded): false at end of stream
             auto carry = [&]() -> bool {
                 if (a[L - 2] > 0) {
@@ -1282,10 +1288,10 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
 #pragma unroll
                     for (int j = 0; j < L - 1; ++j) {
                         if (j == i) a[j] -= 1;
-                        if (j > i) a[j] = r / G.g[j];
+                        if (j > i) a[j] = fdiv(r, wt.gmag[j]);
                         r -= a[j] * G.g[j];
                     }
-                    q = r / m;
+                    q = fdiv(r, mmag);
                     col = r - q * m;
                 }
                 vv = q;
@@ -1316,7 +1322,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                         const uint32_t A = a[L - 2];
                         const uint32_t rin = q * m + col;
                         const uint32_t rl = rin + (uint32_t)lane * g2;
-                        const uint32_t len = ((uint32_t)lane <= A) ? rl / m + 1 : 0u;
+                        const uint32_t len = ((uint32_t)lane <= A) ? fdiv(rl, mmag) + 1 : 0u;
                         uint32_t incl = len;
 #pragma unroll
                         for (int o = 1; o < 32; o <<= 1) {
@@ -1364,7 +1370,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                             }
                             acc_rows += s0 + s1;
                         }
-                        left32 -= __shfl_sync(kFull, incl, nf - 1);
+                        left32 -= __shfl_sync(kFull, incl, (nf - 1) & 31);
                         if (left32 == 0) {
                             more = false;
                             break;
@@ -1372,7 +1378,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                         if ((uint32_t)nf <= A) {   // siblings left at level L-2: a_{L-2} = A - nf
                             a[L - 2] = A - (uint32_t)nf;
                             const uint32_t r2 = rin + (uint32_t)nf * g2;
-                            q = r2 / m;
+                            q = fdiv(r2, mmag);
                             col = r2 - q * m;
                             vv = q;
                         } else {                   // level L-2 exhausted: outer carry
