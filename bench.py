@@ -195,8 +195,18 @@ def run_native(args, rank, world, local_rank):
                 "unit": "GB/s", "algorithmic_bytes_per_launch": alg_bytes}
         roof["frac"] = roof["achieved"] / roof["peak"]
     else:
-        roof = {"kernel": f"k5_walk<{len(g)},{t},count>", "bound": "alu", "achieved": r_local / (k5_ms / 1e3),
-                "unit": "rows/s", "peak": None, "frac": None}
+        # COUNT: one card lookup per leading prefix, 2 B each from the shared-memory copy
+        # of the card table; bound: the shared-memory crossbar, 128 B/clk/SM (B300_MICROARCH.md, LDS/STS)
+        # -> SMs x 128 / 2 lookups per clock at the max SM clock
+        U = leading_prefixes(g, n, len(g) - t)
+        units = U * (W["shard"] + 1) // W["nshards"] - U * W["shard"] // W["nshards"]
+        props = torch.cuda.get_device_properties(dev)
+        clk = sampler.summary().get("sm_max_mhz") or 1965
+        peak = props.multi_processor_count * 128 / 2 * clk * 1e6
+        roof = {"kernel": f"k5_walk<{len(g)},{t},count>", "bound": "alu", "achieved": units / (k5_ms / 1e3),
+                "unit": "card lookups/s (leading prefixes)", "peak": peak,
+                "peak_source": "derived: SMs x 128 B/clk shared-memory crossbar / 2 B per u16 card x max SM clock",
+                "algorithmic_units_per_launch": units, "frac": units / (k5_ms / 1e3) / peak}
     roof["traffic"] = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "k5_traffic.json")))
@@ -291,6 +301,19 @@ def run_e2e(args, spec, local_rank):
     return {"value": tot / el, "unit": UNIT, "h2d_bytes_per_step": 4 * d,
             "d2h_bytes_per_step": (r * d * 4 if mode == "materialize" else 0) + 16, "steps": steps,
             "api": "fz_run_host (gens in host memory -> rows in pinned host memory)"}
+
+
+def leading_prefixes(g, n: int, L: int) -> int:
+    """Leading prefixes (a_1..a_L) with phi <= n = sum_{x<=n} |Z(x; g_1..g_L)| (coin-change counts;
+    measurement bookkeeping for the COUNT roofline, not part of the product path)."""
+    import numpy as np
+
+    c = np.zeros(n + 1, dtype=np.int64)
+    c[0] = 1
+    for gi in g[:L]:
+        for r in range(min(gi, n + 1)):
+            c[r::gi] = np.cumsum(c[r::gi])
+    return int(c.sum())
 
 
 def cpu_baseline(spec, budget_s: float = 12.0):
