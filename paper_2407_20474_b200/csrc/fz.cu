@@ -330,6 +330,36 @@ Gens make_gens(const uint32_t *g, int d)
     return G;
 }
 
+// closed form of Z(x; g, h) for the last two generators g = g_{d-2}, h = g_{d-1} (d >= 2):
+// e = gcd(g, h), g1 = g/e, h1 = h/e, inv = g1^{-1} mod h1 (extended Euclid; 0 when h1 = 1)
+fzk::ProgGens make_prog(const uint32_t *g, int d)
+{
+    fzk::ProgGens P{1, 1, 1, 1, 1, 0};
+    if (d < 2) return P;
+    const uint32_t a = g[d - 2], h = g[d - 1];
+    uint32_t x = a, y = h;
+    while (y) {
+        const uint32_t t = x % y;
+        x = y;
+        y = t;
+    }
+    P.g = a;
+    P.h = h;
+    P.e = x;
+    P.g1 = a / x;
+    P.h1 = h / x;
+    int64_t r0 = P.h1, r1 = P.g1 % P.h1, s0 = 0, s1 = 1;
+    while (r1) {
+        const int64_t q = r0 / r1, r2 = r0 - q * r1, s2 = s0 - q * s1;
+        r0 = r1;
+        r1 = r2;
+        s0 = s1;
+        s1 = s2;
+    }
+    P.inv = P.h1 == 1 ? 0u : (uint32_t)(((s0 % (int64_t)P.h1) + P.h1) % P.h1);
+    return P;
+}
+
 constexpr uint64_t kPlanHeader = 256;
 
 uint64_t max_slices()
@@ -357,12 +387,8 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
         ++g_launches;
         return cuda_check("k3_fill_ring");
     }
-    if (z.fill_mode == 5) {
-        const uint32_t h_last = m->lay->g[z.d - 1];
-        const unsigned blocks = (unsigned)std::min<uint64_t>((z.top + 255) / 256, (uint64_t)device_sms() * 8);
-        fzk::k3_last_level<T><<<std::max(blocks, 1u), 256, 0, s>>>(m->S, m->off, m->rows, z.top, z.ltop, z.L, h_last);
-        ++g_launches;
-        fz_status st = cuda_check("k3_last_level");
+    if (z.fill_mode == 5) {   // the last tail level was written by K2 stage B
+        fz_status st = FZ_OK;
         const unsigned wblocks = (unsigned)std::min<uint64_t>((z.top * 32 + 255) / 256, (uint64_t)device_sms() * 16);
         uint32_t *list = (uint32_t *)(m->ws + z.lay.list);
         for (int i = T - 2; i >= 0 && !st; --i) {
@@ -374,12 +400,8 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
         }
         return st;
     }
-    if (z.fill_mode == 4) {
-        const uint32_t h_last = m->lay->g[z.d - 1];
-        const unsigned blocks = (unsigned)std::min<uint64_t>((z.top + 255) / 256, (uint64_t)device_sms() * 8);
-        fzk::k3_last_level<T><<<std::max(blocks, 1u), 256, 0, s>>>(m->S, m->off, m->rows, z.top, z.ltop, z.L, h_last);
-        ++g_launches;
-        fz_status st = cuda_check("k3_last_level");
+    if (z.fill_mode == 4) {   // the last tail level was written by K2 stage B
+        fz_status st = FZ_OK;
         for (int i = T - 2; i >= 0 && !st; --i) {
             const uint32_t h = m->lay->g[z.L + i];
             const uint64_t cap = std::max<uint64_t>(z.level_block[i], 1);
@@ -567,24 +589,9 @@ fz_status launch_deep_dt(int mode, const WalkArgs &a, const uint64_t *S, uint64_
         ps = std::min(ps, 8);
     }
     // closed form of the last two coordinates (PROG leaves): Z(x; g, h), g = g_{d-2}, h = g_{d-1}
-    fzk::ProgGens P{1, 1, 1, 1, 1, 0};
-    if (D >= 2) {
-        const uint32_t g = a.G.g[D >= 2 ? D - 2 : 0], h = a.G.g[D - 1];
-        uint32_t x = g, y = h;
-        while (y) { const uint32_t t = x % y; x = y; y = t; }
-        P.g = g;
-        P.h = h;
-        P.e = x;
-        P.g1 = g / x;
-        P.h1 = h / x;
-        // inverse of g1 mod h1 (extended Euclid; 0 when h1 = 1)
-        int64_t r0 = P.h1, r1 = P.g1 % P.h1, s0 = 0, s1 = 1;
-        while (r1) {
-            const int64_t q = r0 / r1, r2 = r0 - q * r1, s2 = s0 - q * s1;
-            r0 = r1; r1 = r2; s0 = s1; s1 = s2;
-        }
-        P.inv = P.h1 == 1 ? 0u : (uint32_t)(((s0 % (int64_t)P.h1) + P.h1) % P.h1);
-    }
+    uint32_t gg[D];
+    for (int j = 0; j < D; ++j) gg[j] = a.G.g[j];
+    const fzk::ProgGens P = make_prog(gg, D);
     const uint64_t f0 = a.n / a.G.g[0] + 1;
     const uint32_t f0n = (f0 <= 4096) ? (uint32_t)f0 : 0u;
     kern<<<(unsigned)(device_sms() * ps), fzk::kWalkThreads, (size_t)f0n * 8, s>>>(
@@ -798,6 +805,8 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
     tb.t = z.t;
     tb.link_mode = (z.fill_mode == 1) ? 1 : (z.fill_mode == 2 ? 2 : 0);
     tb.ring_mask = z.ring_rows ? z.ring_rows - 1 : 0;
+    tb.P = make_prog(lay->g, z.d);
+    tb.rows = z.fill_mode ? m->rows : nullptr;
     fz_status st = [&]() -> fz_status {
         FZ_CUDA(cudaMemsetAsync(m->counter, 0, 256, s));
         unsigned int *counter = m->counter;
@@ -806,9 +815,9 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
         const int want = (ge && atoi(ge) > 0) ? atoi(ge) : device_sms();
         const int blocks = std::min(std::min(device_sms(), kMaxGrid), want);
         if (z.fill_mode == 5 && g_fuse_memo) {   // count pass + CSR + default fill in one launch
-            uint32_t *rows = m->rows, *list = (uint32_t *)(m->ws + z.lay.list);
+            uint32_t *list = (uint32_t *)(m->ws + z.lay.list);
             uint64_t cap_list = z.list_cap;
-            void *args5[] = {&G, &tb, &counter, &rows, &list, &cap_list};
+            void *args5[] = {&G, &tb, &counter, &list, &cap_list};
             const void *fn = memo_kernel(z.t);
             if (!fn) return fail(FZ_EINVAL, "t=%d not instantiated", z.t);
             FZ_CUDA(cudaLaunchCooperativeKernel(fn, blocks, 1024, args5, 0, s));

@@ -71,6 +71,29 @@ struct PlanArgs {
     int mode, shard, nshards, L;
 };
 
+struct ProgGens {     // closed form of Z(x; g, h), g = g_{d-2}, h = g_{d-1}
+    uint32_t g, h, e, g1, h1, inv;   // e = gcd(g, h), g1 = g/e, h1 = h/e, inv = g1^{-1} mod h1
+};
+
+// Z(x; g, h) in descending lex order: rows (w0 - j h1, l0 + j g1), j < count
+__device__ __forceinline__ uint32_t prog_block(const ProgGens &P, uint32_t x, uint32_t &w0, uint32_t &l0)
+{
+    if (x % P.e) return 0;
+    const uint32_t ws = (uint32_t)(((uint64_t)((x / P.e) % P.h1) * P.inv) % P.h1);   // w == ws (mod h1)
+    const uint32_t wmax = x / P.g;
+    if (wmax < ws) return 0;
+    w0 = wmax - (wmax - ws) % P.h1;
+    l0 = (x - w0 * P.g) / P.h;
+    return w0 / P.h1 + 1;
+}
+
+// |Z(x; g, h)| in closed form (the count of prog_block)
+__device__ __forceinline__ uint64_t prog_count(const ProgGens &P, uint32_t x)
+{
+    uint32_t w0, l0;
+    return prog_block(P, x, w0, l0);
+}
+
 // Pointers and sizes of the count tables (all in the memo workspace).
 struct Tables {
     uint64_t *S;        // (d+1) x top, natural layout
@@ -87,6 +110,8 @@ struct Tables {
     int d, L, t;
     int link_mode;      // 0 none, 1 u32 ring-relative, 2 u64 absolute
     uint64_t ring_mask;
+    ProgGens P;         // closed form of the last two generators (S_{d-2})
+    uint32_t *rows;     // memo rows (the last tail level is written by K2 stage B), or nullptr
 };
 
 // ------------------------------------------------------------------ helpers
@@ -193,125 +218,6 @@ __device__ void block_column_scan(const uint64_t *src, uint64_t *dst, uint64_t N
             if (k < rows) dst[c + k * g] = run;
         }
         carry += tot;
-    }
-}
-
-// ------------------------------------------------------------------ K1 + K2
-// One cooperative launch (all CTAs co-resident), phases separated by grid barriers:
-//   S_d[x] = [x = 0], W_L[x] = 1;
-//   phase p = 0..d-1: S_{d-1-p} = column scan of S_{d-p} mod g_{d-1-p}, and W_{L-1-p} likewise;
-//   card = S_L, off = exclusive scan of card (two phases), residue-major cardT/offT;
-//   links: per memo row, the source row of the copy-increment (see k3_fill_*).
-__device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigned int *counter, unsigned int &target,
-                                        uint64_t *sm)
-{
-    const uint64_t top = tb.top;
-    const int d = tb.d, L = tb.L, t = d - L;
-    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
-    // Phase 0: the base levels and, in closed form, the first scan of each table:
-    //   S_d[x] = [x = 0], S_{d-1}[x] = [g_{d-1} | x];  W_L[x] = 1, W_{L-1}[x] = floor(x / g_{L-1}) + 1.
-    {
-        const uint64_t gd = G.g[d - 1], gl = L > 0 ? G.g[L - 1] : 1;
-        for (uint64_t x = gt; x < top; x += ng) {
-            tb.S[(uint64_t)d * top + x] = (x == 0) ? 1ull : 0ull;
-            tb.S[(uint64_t)(d - 1) * top + x] = (x % gd == 0) ? 1ull : 0ull;
-            tb.W[(uint64_t)L * top + x] = 1ull;
-            if (L > 0) tb.W[(uint64_t)(L - 1) * top + x] = x / gl + 1;
-        }
-    }
-    // Phases p >= 1: S_{d-1-p} and W_{L-1-p} by column scans (one CTA per residue class), and the
-    // CSR scan of card = S_L as soon as S_L is final (end of phase t-1; phase 0 when t <= 1):
-    // off stage A (per-CTA chunk sums) at phase pa, stage B (chunk scan, off, residue-major copies)
-    // at phase pa + 1.  d - 1 + (extra off phases) grid barriers in total.
-    const int pa = t > 1 ? t : 1;
-    const int nphase = (d > pa + 2) ? d : pa + 2;
-    const uint64_t *card = tb.S + (uint64_t)L * top;
-    const uint64_t CH = (top + gridDim.x - 1) / gridDim.x;
-    const uint64_t c0 = blockIdx.x * CH, c1 = (c0 + CH < top) ? c0 + CH : top;
-    for (int p = 1; p < nphase; ++p) {
-        grid_barrier(counter, target);
-        const int i = d - 1 - p, j = L - 1 - p;
-        const uint64_t gi = i >= 0 ? G.g[i] : 1;
-        const uint64_t ncolS = i >= 0 ? (gi < top ? gi : top) : 0;
-        const uint64_t gj = j >= 0 ? G.g[j] : 1;
-        const uint64_t ncolW = j >= 0 ? (gj < top ? gj : top) : 0;
-        for (uint64_t c = blockIdx.x; c < ncolS + ncolW; c += gridDim.x) {
-            if (c < ncolS)
-                block_column_scan(tb.S + (uint64_t)(i + 1) * top, tb.S + (uint64_t)i * top, top, gi, c, sm);
-            else
-                block_column_scan(tb.W + (uint64_t)(j + 1) * top, tb.W + (uint64_t)j * top, top, gj, c - ncolS, sm);
-        }
-        if (p == pa) {   // K2 stage A: chunk sums of card
-            uint64_t s = 0;
-            for (uint64_t x = c0 + threadIdx.x; x < c1 && x < tb.ltop; x += blockDim.x) s += __ldcg(card + x);
-            uint64_t tot;
-            block_excl_scan(s, sm, &tot);
-            if (threadIdx.x == 0) tb.chunk[blockIdx.x] = tot;
-        }
-        if (p == pa + 1) {   // K2 stage B: off = exclusive scan of card; residue-major cardT / offT
-            uint64_t pre = 0;
-            for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += __ldcg(tb.chunk + b);
-            uint64_t tot;
-            block_excl_scan(pre, sm, &tot);
-            pre = tot;
-            const uint64_t m = tb.m;
-            for (uint64_t xb = c0; xb < c1; xb += blockDim.x) {
-                const uint64_t x = xb + threadIdx.x;
-                const uint64_t c = x < c1 ? __ldcg(card + x) : 0;
-                const uint64_t v = x < tb.ltop ? c : 0;   // CSR over the memo's rows only (x < ltop)
-                uint64_t t2;
-                const uint64_t ex = pre + block_excl_scan(v, sm, &t2);
-                if (x < c1) {
-                    tb.off[x] = ex;
-                    const uint64_t ti = (x % m) * tb.R + x / m;
-                    tb.cardT[ti] = (uint32_t)c;
-                    tb.offT[ti] = ex;
-                    if (x + 1 == top) tb.off[top] = ex + v;
-                }
-                pre += t2;
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned int *counter)
-{
-    __shared__ uint64_t sm[40];
-    unsigned int target = 0;
-    k1_body(G, tb, counter, target, sm);
-    if (tb.link_mode == 0) return;
-    grid_barrier(counter, target);
-    const uint64_t top = tb.top;
-    const int L = tb.L, t = tb.t;
-    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
-    // links: row q of Z(x; tail) lies in block i (0-based tail index) with start
-    // card[x] - S_{L+i}[x] (PAPER.md:163-166, "beginning index of Z_{>=i}"); it is
-    // incr_i of row off[y+1] - S_{L+i}[y] + k of Z(y), y = x - g_{L+i}, k = q - start.
-    const int lane = threadIdx.x & 31;
-    const uint64_t gw = gt >> 5, nw = ng >> 5;
-    if (gw == 0 && lane == 0) {
-        if (tb.link_mode == 1) ((uint32_t *)tb.links)[0] = kZeroLink32;
-        else ((uint64_t *)tb.links)[0] = ~0ull;
-    }
-    for (uint64_t x = 1 + gw; x < top; x += nw) {
-        const uint64_t base = __ldcg(tb.off + x);
-        const uint64_t c = __ldcg(tb.off + x + 1) - base;
-        for (uint64_t q = lane; q < c; q += 32) {
-            int i = 0;
-            uint64_t st = 0;
-            for (int jj = t - 1; jj >= 1; --jj) {
-                uint64_t sj = c - __ldcg(tb.S + (uint64_t)(L + jj) * top + x);
-                if (sj <= q) { i = jj; st = sj; break; }
-            }
-            const uint64_t y = x - G.g[L + i];
-            const uint64_t src = __ldcg(tb.off + y + 1) - __ldcg(tb.S + (uint64_t)(L + i) * top + y) + (q - st);
-            if (tb.link_mode == 1)
-                ((uint32_t *)tb.links)[base + q] = (uint32_t)(src & tb.ring_mask) | ((uint32_t)i << kRingIdxBits);
-            else
-                ((uint64_t *)tb.links)[base + q] = src | ((uint64_t)i << 56);
-        }
     }
 }
 
@@ -862,27 +768,163 @@ __global__ void __launch_bounds__(256) k3_scan_b(const uint64_t *__restrict__ S,
                    ((uint64_t)gridDim.x * blockDim.x) >> 5);
 }
 
-// The whole default memo build in ONE cooperative launch: K1 (count pass + CSR) then the fill-mode-5
-// passes of K3 (last level, then per level: chain lists, blocks), separated by grid barriers instead
-// of kernel boundaries.
+// ------------------------------------------------------------------ K1 + K2 (+ K3 mode 5)
+// One cooperative launch (all CTAs co-resident), phases separated by grid barriers.  Phase 0 writes
+// the closed forms: S_d[x] = [x = 0], S_{d-1}[x] = [g_{d-1} | x], S_{d-2}[x] = |Z(x; g_{d-2}, g_{d-1})|
+// (prog_count), W_L[x] = 1, W_{L-1}[x] = floor(x / g_{L-1}) + 1.  Phase p >= 1 scans S_{d-2-p} and
+// W_{L-1-p} (column scans, one CTA per residue class).  The CSR scan of card = S_L (off, residue-major
+// cardT / offT) takes two phases: chunk sums (stage A) as soon as card is final — phase 0 when t <= 2,
+// since card is then a closed form — and the scan (stage B) one phase later, which also writes the last
+// tail level of every memo block (the row (0,..,0, x / g_{d-1}) at off[x+1] - 1 when g_{d-1} | x).
+// With T >= 2 (fill mode 5 fused) the copy-increment passes follow, one tail level per two phases
+// (chain lists, then blocks), overlapping the leading-level scans still in flight.
 template <int T>
-__global__ void __launch_bounds__(1024) k1_memo(Gens G, Tables tb, unsigned int *counter, uint32_t *rows,
-                                                 uint32_t *list, uint64_t cap_list)
+__device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigned int *counter, unsigned int &target,
+                                        uint64_t *sm, uint32_t *list = nullptr, uint64_t cap_list = 0)
+{
+    const uint64_t top = tb.top, ltop = tb.ltop;
+    const int d = tb.d, L = tb.L, t = d - L;
+    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t gd1 = G.g[d - 1];
+    const uint64_t *card = tb.S + (uint64_t)L * top;
+    auto closed_card = [&](uint64_t x) -> uint64_t {   // card = S_L when t <= 2
+        if (L == d) return x == 0;
+        if (L == d - 1) return x % gd1 == 0;
+        return prog_count(tb.P, (uint32_t)x);
+    };
+    const bool card_closed = t <= 2;
+    const int pa = card_closed ? 0 : (d - 2 - L) + 1;   // stage A: the phase after S_L is final
+    const int pb = pa + 1;                              // stage B (+ last tail level)
+    const int nS = d >= 2 ? d - 2 : 0, nW = L >= 1 ? L - 1 : 0;
+    const int nfill = (T >= 2) ? 2 * (T - 1) : 0;
+    const int last = nS > nW ? (nS > pb + nfill ? nS : pb + nfill) : (nW > pb + nfill ? nW : pb + nfill);
+    const uint64_t CH = (top + gridDim.x - 1) / gridDim.x;
+    const uint64_t c0 = blockIdx.x * CH, c1 = (c0 + CH < top) ? c0 + CH : top;
+    for (int p = 0; p <= last; ++p) {
+        if (p > 0) grid_barrier(counter, target);
+        if (p == 0) {
+            const uint64_t gl = L > 0 ? G.g[L - 1] : 1;
+            for (uint64_t x = gt; x < top; x += ng) {
+                tb.S[(uint64_t)d * top + x] = (x == 0) ? 1ull : 0ull;
+                tb.S[(uint64_t)(d - 1) * top + x] = (x % gd1 == 0) ? 1ull : 0ull;
+                if (d >= 2) tb.S[(uint64_t)(d - 2) * top + x] = prog_count(tb.P, (uint32_t)x);
+                tb.W[(uint64_t)L * top + x] = 1ull;
+                if (L > 0) tb.W[(uint64_t)(L - 1) * top + x] = x / gl + 1;
+            }
+        } else {   // column scans of S_{d-2-p} and W_{L-1-p}
+            const int i = d - 2 - p, j = L - 1 - p;
+            const uint64_t gi = i >= 0 ? G.g[i] : 1;
+            const uint64_t ncolS = i >= 0 ? (gi < top ? gi : top) : 0;
+            const uint64_t gj = j >= 0 ? G.g[j] : 1;
+            const uint64_t ncolW = j >= 0 ? (gj < top ? gj : top) : 0;
+            for (uint64_t c = blockIdx.x; c < ncolS + ncolW; c += gridDim.x) {
+                if (c < ncolS)
+                    block_column_scan(tb.S + (uint64_t)(i + 1) * top, tb.S + (uint64_t)i * top, top, gi, c, sm);
+                else
+                    block_column_scan(tb.W + (uint64_t)(j + 1) * top, tb.W + (uint64_t)j * top, top, gj, c - ncolS,
+                                      sm);
+            }
+        }
+        if (p == pa) {   // K2 stage A: chunk sums of card (memo rows only: x < ltop)
+            uint64_t s = 0;
+            for (uint64_t x = c0 + threadIdx.x; x < c1 && x < ltop; x += blockDim.x)
+                s += card_closed ? closed_card(x) : __ldcg(card + x);
+            uint64_t tot;
+            block_excl_scan(s, sm, &tot);
+            if (threadIdx.x == 0) tb.chunk[blockIdx.x] = tot;
+        }
+        if (p == pb) {   // K2 stage B: off = exclusive scan of card; residue-major cardT / offT; last tail level
+            uint64_t pre = 0;
+            for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += __ldcg(tb.chunk + b);
+            uint64_t tot;
+            block_excl_scan(pre, sm, &tot);
+            pre = tot;
+            const uint64_t m = tb.m;
+            for (uint64_t xb = c0; xb < c1; xb += blockDim.x) {
+                const uint64_t x = xb + threadIdx.x;
+                const uint64_t c = x < c1 ? __ldcg(card + x) : 0;
+                const uint64_t v = x < ltop ? c : 0;   // CSR over the memo's rows only (x < ltop)
+                uint64_t t2;
+                const uint64_t ex = pre + block_excl_scan(v, sm, &t2);
+                if (x < c1) {
+                    tb.off[x] = ex;
+                    const uint64_t ti = (x % m) * tb.R + x / m;
+                    tb.cardT[ti] = (uint32_t)c;
+                    tb.offT[ti] = ex;
+                    if (x + 1 == top) tb.off[top] = ex + v;
+                    if (tb.rows && t >= 1 && x < ltop && x % gd1 == 0) {   // block t-1 of Z(x): [(0,..,0, x/h)]
+                        uint32_t *o = tb.rows + (ex + v - 1) * (uint64_t)t;
+                        for (int w = 0; w < t - 1; ++w) o[w] = 0;
+                        o[t - 1] = (uint32_t)(x / gd1);
+                    }
+                }
+                pre += t2;
+            }
+        }
+        if constexpr (T >= 2) {   // fill mode 5: level i = T-2 .. 0, chain lists then blocks
+            if (p > pb && p <= pb + nfill) {
+                const int k = p - pb - 1, i = T - 2 - k / 2;
+                const uint32_t h = G.g[L + i];
+                if (k % 2 == 0)
+                    scan_a_body<T>(tb.S, tb.off, tb.rows, list, cap_list, top, ltop, L, i, h, gt >> 5, ng >> 5);
+                else
+                    scan_b_body<T>(tb.S, tb.off, tb.rows, list, cap_list, top, ltop, L, i, h, gt >> 5, ng >> 5);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned int *counter)
 {
     __shared__ uint64_t sm[40];
     unsigned int target = 0;
-    k1_body(G, tb, counter, target, sm);
+    k1_body<0>(G, tb, counter, target, sm);
+    if (tb.link_mode == 0) return;
+    grid_barrier(counter, target);
+    const uint64_t top = tb.top;
+    const int L = tb.L, t = tb.t;
     const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
-    grid_barrier(counter, target);
-    last_level_body<T>(tb.S, tb.off, rows, tb.top, tb.ltop, tb.L, G.g[tb.d - 1], gt, ng);
-    for (int i = T - 2; i >= 0; --i) {
-        const uint32_t h = G.g[tb.L + i];
-        grid_barrier(counter, target);
-        scan_a_body<T>(tb.S, tb.off, rows, list, cap_list, tb.top, tb.ltop, tb.L, i, h, gt >> 5, ng >> 5);
-        grid_barrier(counter, target);
-        scan_b_body<T>(tb.S, tb.off, rows, list, cap_list, tb.top, tb.ltop, tb.L, i, h, gt >> 5, ng >> 5);
+    // links: row q of Z(x; tail) lies in block i (0-based tail index) with start
+    // card[x] - S_{L+i}[x] (PAPER.md:163-166, "beginning index of Z_{>=i}"); it is
+    // incr_i of row off[y+1] - S_{L+i}[y] + k of Z(y), y = x - g_{L+i}, k = q - start.
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = gt >> 5, nw = ng >> 5;
+    if (gw == 0 && lane == 0) {
+        if (tb.link_mode == 1) ((uint32_t *)tb.links)[0] = kZeroLink32;
+        else ((uint64_t *)tb.links)[0] = ~0ull;
     }
+    for (uint64_t x = 1 + gw; x < top; x += nw) {
+        const uint64_t base = __ldcg(tb.off + x);
+        const uint64_t c = __ldcg(tb.off + x + 1) - base;
+        for (uint64_t q = lane; q < c; q += 32) {
+            int i = 0;
+            uint64_t st = 0;
+            for (int jj = t - 1; jj >= 1; --jj) {
+                uint64_t sj = c - __ldcg(tb.S + (uint64_t)(L + jj) * top + x);
+                if (sj <= q) { i = jj; st = sj; break; }
+            }
+            const uint64_t y = x - G.g[L + i];
+            const uint64_t src = __ldcg(tb.off + y + 1) - __ldcg(tb.S + (uint64_t)(L + i) * top + y) + (q - st);
+            if (tb.link_mode == 1)
+                ((uint32_t *)tb.links)[base + q] = (uint32_t)(src & tb.ring_mask) | ((uint32_t)i << kRingIdxBits);
+            else
+                ((uint64_t *)tb.links)[base + q] = src | ((uint64_t)i << 56);
+        }
+    }
+}
+
+// The whole default memo build in ONE cooperative launch: K1 (count pass + CSR + last tail level) and
+// the fill-mode-5 passes of K3 (per tail level: chain lists, blocks), separated by grid barriers
+// instead of kernel boundaries.
+template <int T>
+__global__ void __launch_bounds__(1024) k1_memo(Gens G, Tables tb, unsigned int *counter, uint32_t *list,
+                                                 uint64_t cap_list)
+{
+    __shared__ uint64_t sm[40];
+    unsigned int target = 0;
+    k1_body<T>(G, tb, counter, target, sm, list, cap_list);
 }
 
 // Fill mode 2: one CTA, sources read back through L2 (window too large for the
@@ -1548,22 +1590,6 @@ __device__ __forceinline__ uint32_t sel_u32(const uint32_t (&v)[N], int k)
 
 // BlockInfo.memo_row of a computed leaf: flag bits, then two 30-bit coordinates
 constexpr uint64_t kComputed = 1ull << 63, kProg = 1ull << 62;
-
-struct ProgGens {     // closed form of Z(x; g, h), g = g_{d-2}, h = g_{d-1}
-    uint32_t g, h, e, g1, h1, inv;   // e = gcd(g, h), g1 = g/e, h1 = h/e, inv = g1^{-1} mod h1
-};
-
-// Z(x; g, h) in descending lex order: rows (w0 - j h1, l0 + j g1), j < count
-__device__ __forceinline__ uint32_t prog_block(const ProgGens &P, uint32_t x, uint32_t &w0, uint32_t &l0)
-{
-    if (x % P.e) return 0;
-    const uint32_t ws = (uint32_t)(((uint64_t)((x / P.e) % P.h1) * P.inv) % P.h1);   // w == ws (mod h1)
-    const uint32_t wmax = x / P.g;
-    if (wmax < ws) return 0;
-    w0 = wmax - (wmax - ws) % P.h1;
-    l0 = (x - w0 * P.g) / P.h;
-    return w0 / P.h1 + 1;
-}
 
 template <int D, int T, int MODE>
 __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, PlanHdr *hdr,
