@@ -271,36 +271,76 @@ def count_mode_extra(local_rank):
     return res
 
 
-def run_e2e(args, spec, local_rank):
-    """Same metric through the C-ABI whole-path call with HOST buffers (fz_run_host)."""
+def run_e2e(args, spec, W, rank, world, local_rank):
+    """Same metric end to end through the public API from HOST buffers, on every rank; the timed region
+    (barrier-bracketed, max over ranks) holds each step's H2D of the generator tuple and D2H of the result.
+    MATERIALIZE (weak, one element per rank): fz_run_host, rows streamed into pinned host memory.
+    COUNT (strong, one problem cut into shards): this rank's shard through Layout/Memo/Plan with the
+    NCCL all_reduce of {rows, hash}, then the 16-byte D2H read of the global result."""
     import torch
+    import torch.distributed as dist
 
     from paper_2407_20474_b200 import fz
 
     g, n, t, mode = spec
-    lay = fz.Layout(g, t, n + 1, entries=mode != "count")
-    rows = None
-    host = None
-    ws = torch.empty(fz.run_workspace_bytes(g, t, n, mode), dtype=torch.uint8, device="cuda")
-    if mode == "materialize":
-        from paper_2407_20474_b200.fz import Memo, Plan  # noqa: F401
-        m = fz.Memo(layout=lay)
-        rows = fz.Plan(m, n, mode).rows
-        del m
-        host = torch.empty((rows, len(g)), dtype=torch.int32).pin_memory()
-    fz.run_host(g, t, n, mode, host, workspace=ws)       # warm-up
-    torch.cuda.synchronize()
+    d = len(g)
+    dev = torch.device("cuda", local_rank)
     steps = max(1, min(args.steps, 3))
+    host = None
+    if mode == "materialize":
+        ws = torch.empty(fz.run_workspace_bytes(g, t, n, mode), dtype=torch.uint8, device=dev)
+        lay = fz.Layout(g, t, n + 1, entries=True)
+        rows = fz.Plan(fz.Memo(layout=lay), n, mode).rows
+        host = torch.empty((rows, d), dtype=torch.int32).pin_memory()
+
+        def one():
+            return fz.run_host(g, t, n, mode, host, workspace=ws)[0]
+    else:
+        lay = fz.Layout(g, t, n + 1, entries=False)
+        ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device=dev)
+        pws = None
+        g_host = torch.tensor(list(g), dtype=torch.int32).pin_memory()
+        g_dev = torch.empty_like(g_host, device=dev)
+
+        def one():
+            nonlocal pws
+            g_dev.copy_(g_host, non_blocking=True)          # the step's input, H2D
+            m = fz.Memo(layout=lay, workspace=ws)
+            if pws is None:
+                pws = torch.empty(fz.plan_workspace_bytes(m), dtype=torch.uint8, device=dev)
+            p = fz.Plan(m, n, mode, W["shard"], W["nshards"], workspace=pws)
+            p.launch()
+            if world > 1:
+                dist.all_reduce(p.result_tensor(), op=dist.ReduceOp.SUM)
+            return p.result()[0]                            # D2H of {rows, hash}
+    one()                                                   # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     tot = 0
     for _ in range(steps):
-        r, _h = fz.run_host(g, t, n, mode, host, workspace=ws)
-        tot += r
-    el = time.perf_counter() - t0
-    d = len(g)
-    return {"value": tot / el, "unit": UNIT, "h2d_bytes_per_step": 4 * d,
-            "d2h_bytes_per_step": (r * d * 4 if mode == "materialize" else 0) + 16, "steps": steps,
-            "api": "fz_run_host (gens in host memory -> rows in pinned host memory)"}
+        tot += one()
+    torch.cuda.synchronize()
+    el = torch.tensor([time.perf_counter() - t0, float(tot)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        mx = el.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = el.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        el_s = float(mx[0])
+        tot = float(sm[1]) if W["scaling"] == "weak" else float(el[1])   # strong: all_reduced already
+    else:
+        el_s = float(el[0])
+    local_rows = int(el[1].item()) // steps
+    return {"value": tot / el_s, "unit": UNIT, "h2d_bytes_per_step": 4 * d,
+            "d2h_bytes_per_step": (local_rows * d * 4 if mode == "materialize" else 0) + 16,
+            "bytes_per": "rank and step",
+            "steps": steps, "timing": "host wall clock around synchronised steps, max over ranks",
+            "api": ("fz_run_host (gens in host memory -> rows in pinned host memory), one element per rank"
+                    if mode == "materialize" else
+                    "Layout/Memo/Plan (gens H2D each step) + all_reduce + fz_plan_result (16 B D2H)")}
 
 
 def leading_prefixes(g, n: int, L: int) -> int:
@@ -419,13 +459,9 @@ def main():
         else:
             dist.init_process_group(backend)
     res, spec = run_native(args, rank, world, local_rank)
+    if not args.no_e2e:
+        res["e2e"] = run_e2e(args, spec, workload(args.config, rank, world), rank, world, local_rank)
     if rank == 0:
-        if not args.no_e2e:
-            e2e = run_e2e(args, spec, local_rank)
-            if world > 1 and res["scaling"] == "weak":
-                e2e["value"] *= world
-                e2e["note"] = "rank 0's end-to-end rate x N (independent elements per GPU)"
-            res["e2e"] = e2e
         if world == 1 and not args.no_cpu:
             res["cpu_baseline"] = cpu_baseline(spec)
         if world == 1 and args.config == "C2" and not args.no_count:

@@ -1,7 +1,7 @@
 """Summarise ncu outputs into profiles/ (committed evidence).
 
   python tools/ncu_summary.py launches <launches.csv> <out.md>     # --metrics gpu__time_duration.sum list
-  python tools/ncu_summary.py full <report.ncu-rep> <out.md> [key]  # --set full capture (one or more kernels)
+  python tools/ncu_summary.py full <report.ncu-rep | raw.csv> <out.md> [key]  # --set full capture (one or more kernels)
 
 `full` also merges {key: {dram_bytes_per_launch, ...}} into profiles/k5_traffic.json.
 """
@@ -44,7 +44,10 @@ def launches(path, out):
 
 
 def full(rep, out, key=None):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):   # `ncu -i X.ncu-rep --page raw --csv` exported on the GPU box
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rd = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rd[0], rd[1], rd[2:]
     want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
