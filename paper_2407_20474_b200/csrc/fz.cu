@@ -128,6 +128,7 @@ struct Sizing {
     uint64_t level_block[FZ_MAX_D] = {0};   // fill mode 4: largest block i of any Z(x), per tail level
     uint64_t list_cap = 0;                   // fill mode 5: rows per chain list (max_x S_{L+i}[x] over levels)
     uint64_t list_bytes = 0;
+    uint8_t lg_a[FZ_MAX_D] = {0}, lg_b[FZ_MAX_D] = {0};   // fill mode 5: log2 lanes per x, per level and pass
     uint64_t smem_bytes = 0;    // fill mode 1: dynamic shared memory
     int fill_mode = 0;
     Layout lay{};
@@ -262,6 +263,24 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
             chains_max = std::max<uint64_t>(chains_max, std::min<uint64_t>(g[L + i], ltop));
         }
         z.list_bytes = chains_max * z.list_cap * 4ull * t;
+        // lanes per x of the two passes of level i: a whole warp per x (coalesced row copies), except
+        // a single lane per x for chain-list passes averaging at most one row per x (measured with
+        // tools/k1_trace.py: smaller groups lose coalescing on the block passes)
+        auto pick_lg = [&](double rows_per_x, bool chain_pass) -> uint8_t {
+            return (chain_pass && rows_per_x <= 1.0) ? 0 : 5;
+        };
+        for (int i = 0; i + 1 < t; ++i) {
+            const uint64_t *Si = H.S.data() + (size_t)(L + i) * top, *Si1 = Si + top;
+            double sa = 0, sb = 0;
+            for (uint64_t x = 0; x < ltop; ++x) {
+                sa += double(Si1[x]);
+                sb += double(Si[x] - Si1[x]);
+            }
+            z.lg_a[i] = pick_lg(sa / double(std::max<uint64_t>(ltop, 1)), true);
+            z.lg_b[i] = pick_lg(sb / double(std::max<uint64_t>(ltop, 1)), false);
+            const char *fl = getenv("FZ_SCAN_LG");   // tuning override: log2 lanes per x in both passes
+            if (fl && *fl && atoi(fl) >= 0 && atoi(fl) <= 5) z.lg_a[i] = z.lg_b[i] = (uint8_t)atoi(fl);
+        }
         const int forced = g_fill_override;
         // modes 1-4 fill the whole table range; a partial memo (ltop < top) takes mode 5
         if (forced >= 1 && forced <= 5 && !(forced == 1 && !fit) && !(forced == 4 && !chains_fit) &&
@@ -334,7 +353,7 @@ Gens make_gens(const uint32_t *g, int d)
 // e = gcd(g, h), g1 = g/e, h1 = h/e, inv = g1^{-1} mod h1 (extended Euclid; 0 when h1 = 1)
 fzk::ProgGens make_prog(const uint32_t *g, int d)
 {
-    fzk::ProgGens P{1, 1, 1, 1, 1, 0};
+    fzk::ProgGens P{1, 1, 1, 1, 1, 0, 0, 0, 0, 0};
     if (d < 2) return P;
     const uint32_t a = g[d - 2], h = g[d - 1];
     uint32_t x = a, y = h;
@@ -357,6 +376,11 @@ fzk::ProgGens make_prog(const uint32_t *g, int d)
         s1 = s2;
     }
     P.inv = P.h1 == 1 ? 0u : (uint32_t)(((s0 % (int64_t)P.h1) + P.h1) % P.h1);
+    auto magic = [](uint32_t v) -> uint64_t { return v == 1 ? 0ull : ~0ull / v + 1; };   // ceil(2^64 / v)
+    P.mg = magic(P.g);
+    P.mh = magic(P.h);
+    P.me = magic(P.e);
+    P.mh1 = magic(P.h1);
     return P;
 }
 
@@ -393,8 +417,10 @@ fz_status launch_fill_t(const fz_memo *m, cudaStream_t s)
         uint32_t *list = (uint32_t *)(m->ws + z.lay.list);
         for (int i = T - 2; i >= 0 && !st; --i) {
             const uint32_t h = m->lay->g[z.L + i];
-            fzk::k3_scan_a<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.ltop, z.L, i, h);
-            fzk::k3_scan_b<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.ltop, z.L, i, h);
+            fzk::k3_scan_a<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.ltop, z.L, i, h,
+                                                      z.lg_a[i]);
+            fzk::k3_scan_b<T><<<wblocks, 256, 0, s>>>(m->S, m->off, m->rows, list, z.list_cap, z.top, z.ltop, z.L, i, h,
+                                                      z.lg_b[i]);
             g_launches += 2;
             st = cuda_check("k3_scan");
         }
@@ -807,6 +833,14 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
     tb.ring_mask = z.ring_rows ? z.ring_rows - 1 : 0;
     tb.P = make_prog(lay->g, z.d);
     tb.rows = z.fill_mode ? m->rows : nullptr;
+    {   // diagnostics: FZ_K1_TRACE = device address of a u64[grid * 32] buffer for phase timestamps
+        const char *tr = getenv("FZ_K1_TRACE");
+        tb.trace = (tr && *tr) ? (uint64_t *)(uintptr_t)strtoull(tr, nullptr, 0) : nullptr;
+    }
+    for (int i = 0; i < FZ_MAX_D; ++i) {
+        tb.lg_a[i] = z.lg_a[i];
+        tb.lg_b[i] = z.lg_b[i];
+    }
     fz_status st = [&]() -> fz_status {
         FZ_CUDA(cudaMemsetAsync(m->counter, 0, 256, s));
         unsigned int *counter = m->counter;

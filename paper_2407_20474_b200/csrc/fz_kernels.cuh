@@ -71,20 +71,34 @@ struct PlanArgs {
     int mode, shard, nshards, L;
 };
 
+// x / g for x < 2^32 by the precomputed magic M = ceil(2^64 / g) (M = 0 encodes g = 1): the error of
+// x M / 2^64 against x / g is below x / 2^64 < 1 / g, so the floor is exact.
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint64_t M) { return M ? (uint32_t)__umul64hi(x, M) : x; }
+
 struct ProgGens {     // closed form of Z(x; g, h), g = g_{d-2}, h = g_{d-1}
     uint32_t g, h, e, g1, h1, inv;   // e = gcd(g, h), g1 = g/e, h1 = h/e, inv = g1^{-1} mod h1
+    uint64_t mg, mh, me, mh1;        // fdiv magics of g, h, e, h1 (0 encodes 1)
 };
 
 // Z(x; g, h) in descending lex order: rows (w0 - j h1, l0 + j g1), j < count
 __device__ __forceinline__ uint32_t prog_block(const ProgGens &P, uint32_t x, uint32_t &w0, uint32_t &l0)
 {
-    if (x % P.e) return 0;
-    const uint32_t ws = (uint32_t)(((uint64_t)((x / P.e) % P.h1) * P.inv) % P.h1);   // w == ws (mod h1)
-    const uint32_t wmax = x / P.g;
+    const uint32_t xe = fdiv(x, P.me);
+    if (x != xe * P.e) return 0;
+    const uint32_t a = xe - fdiv(xe, P.mh1) * P.h1;          // (x / e) mod h1
+    uint32_t ws;                                               // w == ws (mod h1)
+    if (P.h1 <= 0xffffu) {
+        const uint32_t pr = a * P.inv;                         // < h1^2 < 2^32
+        ws = pr - fdiv(pr, P.mh1) * P.h1;
+    } else {
+        ws = (uint32_t)(((uint64_t)a * P.inv) % P.h1);
+    }
+    const uint32_t wmax = fdiv(x, P.mg);
     if (wmax < ws) return 0;
-    w0 = wmax - (wmax - ws) % P.h1;
-    l0 = (x - w0 * P.g) / P.h;
-    return w0 / P.h1 + 1;
+    const uint32_t dw = wmax - ws;
+    w0 = wmax - (dw - fdiv(dw, P.mh1) * P.h1);
+    l0 = fdiv(x - w0 * P.g, P.mh);
+    return fdiv(w0, P.mh1) + 1;
 }
 
 // |Z(x; g, h)| in closed form (the count of prog_block)
@@ -112,6 +126,8 @@ struct Tables {
     uint64_t ring_mask;
     ProgGens P;         // closed form of the last two generators (S_{d-2})
     uint32_t *rows;     // memo rows (the last tail level is written by K2 stage B), or nullptr
+    uint8_t lg_a[kMaxD], lg_b[kMaxD];   // fill mode 5: log2 lanes per x of the chain-list / block passes, per level
+    uint64_t *trace;    // diagnostics: per-CTA phase timestamps [grid][16][2] (FZ_K1_TRACE), or nullptr
 };
 
 // ------------------------------------------------------------------ helpers
@@ -192,8 +208,10 @@ __device__ __forceinline__ void grid_barrier(unsigned int *counter, unsigned int
 }
 
 // Inclusive scan down one residue column c of a level:
-//   dst[x] = src[x] + dst[x - g]  for x = c, c+g, c+2g, ... < N.   One CTA.
-__device__ void block_column_scan(const uint64_t *src, uint64_t *dst, uint64_t N, uint64_t g, uint64_t c, uint64_t *sm)
+//   dst[x] = src(x) + dst[x - g]  for x = c, c+g, c+2g, ... < N.   One CTA.  src is a table in memory
+// or a closed form evaluated on the fly (the scans whose source level is closed run in phase 0).
+template <class Src>
+__device__ void block_column_scan_f(Src src, uint64_t *dst, uint64_t N, uint64_t g, uint64_t c, uint64_t *sm)
 {
     constexpr int E = 8;
     const uint64_t rows = (N - c + g - 1) / g;
@@ -206,7 +224,7 @@ __device__ void block_column_scan(const uint64_t *src, uint64_t *dst, uint64_t N
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const uint64_t k = kb + e;
-            v[e] = k < rows ? __ldcg(src + c + k * g) : 0;
+            v[e] = k < rows ? src(c + k * g) : 0;
             s += v[e];
         }
         uint64_t tot;
@@ -219,6 +237,11 @@ __device__ void block_column_scan(const uint64_t *src, uint64_t *dst, uint64_t N
         }
         carry += tot;
     }
+}
+
+__device__ void block_column_scan(const uint64_t *src, uint64_t *dst, uint64_t N, uint64_t g, uint64_t c, uint64_t *sm)
+{
+    block_column_scan_f([=](uint64_t x) { return __ldcg(src + x); }, dst, N, g, c, sm);
 }
 
 template <int T>
@@ -698,94 +721,158 @@ __global__ void __launch_bounds__(512) k3_chain(const uint64_t *__restrict__ S, 
 //   phase B: block_i(Z(x)) = list prefix of length S_i[x] - S_{i+1}[x], + (x div h) e_i
 //            (= incr_i applied x div h - j' times to the row appended at position j')
 // -- the same copy-and-increment results, with no dependency between x values inside a pass.
+// Rows are copied by groups of G = 2^lg lanes (one group per x; lg chosen per level by the host from
+// the level's mean rows per x, so the common few-row blocks do not idle a whole warp), U rows per lane
+// loaded before any is stored (U loads in flight instead of one dependent round trip per row).
+template <int T>
+__device__ __forceinline__ void copy_incr(const uint32_t *__restrict__ src, uint32_t *__restrict__ dst, uint32_t n,
+                                          uint32_t lane, uint32_t G, int i, uint32_t delta)
+{
+    constexpr int U = 4;
+    auto ld = [&](uint32_t k, uint32_t (&v)[T]) {
+        if constexpr (T == 2) {
+            const uint2 w = __ldcg(reinterpret_cast<const uint2 *>(src) + k);
+            v[0] = w.x;
+            v[1] = w.y;
+        } else if constexpr (T == 4) {
+            const uint4 w = __ldcg(reinterpret_cast<const uint4 *>(src) + k);
+            v[0] = w.x;
+            v[1] = w.y;
+            v[2] = w.z;
+            v[3] = w.w;
+        } else {
+#pragma unroll
+            for (int w = 0; w < T; ++w) v[w] = __ldcg(src + (uint64_t)k * T + w);
+        }
+    };
+    auto st = [&](uint32_t k, uint32_t (&v)[T]) {
+#pragma unroll
+        for (int w = 0; w < T; ++w) v[w] += (w == i) ? delta : 0u;
+        if constexpr (T == 2) {
+            reinterpret_cast<uint2 *>(dst)[k] = make_uint2(v[0], v[1]);
+        } else if constexpr (T == 4) {
+            reinterpret_cast<uint4 *>(dst)[k] = make_uint4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int w = 0; w < T; ++w) dst[(uint64_t)k * T + w] = v[w];
+        }
+    };
+    for (uint32_t k = lane; k < n; k += U * G) {   // one batch: up to U rows per lane, loads before stores
+        uint32_t v[U][T];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k + u * G < n) ld(k + u * G, v[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k + u * G < n) st(k + u * G, v[u]);
+    }
+}
+
+// gg / ng: this lane's group index and the number of groups; lane: index within the group of G lanes.
 template <int T>
 __device__ __forceinline__ void scan_a_body(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                             const uint32_t *rows, uint32_t *list, uint64_t cap_list, uint64_t top,
-                                            uint64_t ltop, int L, int i, uint32_t h, uint64_t gw, uint64_t nw)
+                                            uint64_t ltop, int L, int i, uint32_t h, uint64_t gg, uint64_t ng,
+                                            uint32_t lane, uint32_t G)
 {
-    const int lane = threadIdx.x & 31;
     const uint64_t *Si = S + (uint64_t)(L + i) * top, *Si1 = Si + top;
-    for (uint64_t x = gw; x + h < ltop; x += nw) {
-        const uint64_t ns = __ldg(Si1 + x);
-        if (ns == 0) continue;
-        const uint64_t so = __ldg(off + x + 1) - ns, base = __ldg(Si + x) - ns;
-        const uint32_t j = (uint32_t)(x / h), r = (uint32_t)(x - (uint64_t)j * h);
-        uint32_t *lr = list + ((uint64_t)r * cap_list + base) * T;
-        for (uint64_t k = lane; k < ns; k += 32) {
-            const uint32_t *src = rows + (so + k) * T;
-#pragma unroll
-            for (int w = 0; w < T; ++w) lr[k * T + w] = __ldcg(src + w) - (w == i ? j : 0u);
+    // rounds of ng consecutive x, assigned in alternating direction (block sizes grow with x)
+    uint64_t k = 0, x = gg;
+    if (x + h >= ltop) return;
+    uint64_t ns = __ldg(Si1 + x), o1 = __ldg(off + x + 1), si = __ldg(Si + x);
+    for (;;) {   // the next x's header is loaded before this x's rows are copied
+        ++k;
+        const uint64_t xn = k * ng + ((k & 1) ? ng - 1 - gg : gg);
+        const bool more = xn + h < ltop;
+        uint64_t nsn = 0, o1n = 0, sin = 0;
+        if (more) {
+            nsn = __ldg(Si1 + xn);
+            o1n = __ldg(off + xn + 1);
+            sin = __ldg(Si + xn);
         }
+        if (ns) {
+            const uint64_t so = o1 - ns, base = si - ns;
+            const uint32_t j = (uint32_t)x / h, r = (uint32_t)x - j * h;   // x < top <= 2^28
+            copy_incr<T>(rows + so * T, list + ((uint64_t)r * cap_list + base) * T, (uint32_t)ns, lane, G, i, 0u - j);
+        }
+        if (!more) break;
+        x = xn;
+        ns = nsn;
+        o1 = o1n;
+        si = sin;
     }
 }
 
 template <int T>
 __device__ __forceinline__ void scan_b_body(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                             uint32_t *rows, const uint32_t *list, uint64_t cap_list, uint64_t top,
-                                            uint64_t ltop, int L, int i, uint32_t h, uint64_t gw, uint64_t nw)
+                                            uint64_t ltop, int L, int i, uint32_t h, uint64_t gg, uint64_t ng,
+                                            uint32_t lane, uint32_t G)
 {
-    const int lane = threadIdx.x & 31;
     const uint64_t *Si = S + (uint64_t)(L + i) * top, *Si1 = Si + top;
-    for (uint64_t x = h + gw; x < ltop; x += nw) {
-        const uint64_t si = __ldg(Si + x);
-        const uint64_t nb = si - __ldg(Si1 + x);
-        if (nb == 0) continue;
-        const uint64_t dst = __ldg(off + x + 1) - si;
-        const uint32_t c = (uint32_t)(x / h), r = (uint32_t)(x - (uint64_t)c * h);
-        const uint32_t *lr = list + (uint64_t)r * cap_list * T;
-        for (uint64_t q = lane; q < nb; q += 32) {
-            uint32_t v[T];
-#pragma unroll
-            for (int w = 0; w < T; ++w) v[w] = __ldcg(lr + q * T + w) + (w == i ? c : 0u);
-            uint32_t *o = rows + (dst + q) * T;
-            if constexpr (T == 2) {
-                *reinterpret_cast<uint2 *>(o) = make_uint2(v[0], v[1]);
-            } else if constexpr (T == 4) {
-                *reinterpret_cast<uint4 *>(o) = make_uint4(v[0], v[1], v[2], v[3]);
-            } else {
-#pragma unroll
-                for (int w = 0; w < T; ++w) o[w] = v[w];
-            }
+    uint64_t k = 0, x = h + gg;
+    if (x >= ltop) return;
+    uint64_t si = __ldg(Si + x), s1 = __ldg(Si1 + x), o1 = __ldg(off + x + 1);
+    for (;;) {   // the next x's header is loaded before this x's rows are copied
+        ++k;
+        const uint64_t xn = h + k * ng + ((k & 1) ? ng - 1 - gg : gg);
+        const bool more = xn < ltop;
+        uint64_t sin = 0, s1n = 0, o1n = 0;
+        if (more) {
+            sin = __ldg(Si + xn);
+            s1n = __ldg(Si1 + xn);
+            o1n = __ldg(off + xn + 1);
         }
+        const uint64_t nb = si - s1;
+        if (nb) {
+            const uint32_t c = (uint32_t)x / h, r = (uint32_t)x - c * h;
+            copy_incr<T>(list + (uint64_t)r * cap_list * T, rows + (o1 - si) * T, (uint32_t)nb, lane, G, i, c);
+        }
+        if (!more) break;
+        x = xn;
+        si = sin;
+        s1 = s1n;
+        o1 = o1n;
     }
 }
 
 template <int T>
 __global__ void __launch_bounds__(256) k3_scan_a(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                                   const uint32_t *rows, uint32_t *list, uint64_t cap_list, uint64_t top,
-                                                  uint64_t ltop, int L, int i, uint32_t h)
+                                                  uint64_t ltop, int L, int i, uint32_t h, int lg)
 {
-    scan_a_body<T>(S, off, rows, list, cap_list, top, ltop, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
-                   ((uint64_t)gridDim.x * blockDim.x) >> 5);
+    scan_a_body<T>(S, off, rows, list, cap_list, top, ltop, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> lg,
+                   ((uint64_t)gridDim.x * blockDim.x) >> lg, threadIdx.x & ((1u << lg) - 1), 1u << lg);
 }
 
 template <int T>
 __global__ void __launch_bounds__(256) k3_scan_b(const uint64_t *__restrict__ S, const uint64_t *__restrict__ off,
                                                   uint32_t *rows, const uint32_t *list, uint64_t cap_list, uint64_t top,
-                                                  uint64_t ltop, int L, int i, uint32_t h)
+                                                  uint64_t ltop, int L, int i, uint32_t h, int lg)
 {
-    scan_b_body<T>(S, off, rows, list, cap_list, top, ltop, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
-                   ((uint64_t)gridDim.x * blockDim.x) >> 5);
+    scan_b_body<T>(S, off, rows, list, cap_list, top, ltop, L, i, h, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> lg,
+                   ((uint64_t)gridDim.x * blockDim.x) >> lg, threadIdx.x & ((1u << lg) - 1), 1u << lg);
 }
 
 // ------------------------------------------------------------------ K1 + K2 (+ K3 mode 5)
 // One cooperative launch (all CTAs co-resident), phases separated by grid barriers.  Phase 0 writes
 // the closed forms: S_d[x] = [x = 0], S_{d-1}[x] = [g_{d-1} | x], S_{d-2}[x] = |Z(x; g_{d-2}, g_{d-1})|
-// (prog_count), W_L[x] = 1, W_{L-1}[x] = floor(x / g_{L-1}) + 1.  Phase p >= 1 scans S_{d-2-p} and
-// W_{L-1-p} (column scans, one CTA per residue class).  The CSR scan of card = S_L (off, residue-major
-// cardT / offT) takes two phases: chunk sums (stage A) as soon as card is final — phase 0 when t <= 2,
-// since card is then a closed form — and the scan (stage B) one phase later, which also writes the last
-// tail level of every memo block (the row (0,..,0, x / g_{d-1}) at off[x+1] - 1 when g_{d-1} | x).
-// With T >= 2 (fill mode 5 fused) the copy-increment passes follow, one tail level per two phases
-// (chain lists, then blocks), overlapping the leading-level scans still in flight.
+// (prog_count), W_L[x] = 1, W_{L-1}[x] = floor(x / g_{L-1}) + 1.  Phase p >= 0 scans S_{d-3-p} and
+// W_{L-2-p} (column scans, one CTA per residue class; in phase 0 their sources are the closed forms,
+// evaluated on the fly).  The CSR scan of card = S_L (off, residue-major cardT / offT) takes two
+// phases: chunk sums (stage A) as soon as card is final — phase 0 when t <= 2, since card is then a
+// closed form — and the scan (stage B) one phase later, which also writes the last tail level of every
+// memo block (the row (0,..,0, x / g_{d-1}) at off[x+1] - 1 when g_{d-1} | x).  With T >= 2 (fill
+// mode 5 fused) the copy-increment passes follow, one tail level per two phases (chain lists, then
+// blocks), overlapping the leading-level scans still in flight.  The column scans take the leading
+// CTAs; stage A / B chunks, the fill passes and the elementwise closed forms go to the other CTAs
+// when the scans leave at least half the grid free.
 template <int T>
 __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigned int *counter, unsigned int &target,
                                         uint64_t *sm, uint32_t *list = nullptr, uint64_t cap_list = 0)
 {
     const uint64_t top = tb.top, ltop = tb.ltop;
     const int d = tb.d, L = tb.L, t = d - L;
-    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t gd1 = G.g[d - 1];
     const uint64_t *card = tb.S + (uint64_t)L * top;
     auto closed_card = [&](uint64_t x) -> uint64_t {   // card = S_L when t <= 2
@@ -794,49 +881,92 @@ __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigne
         return prog_count(tb.P, (uint32_t)x);
     };
     const bool card_closed = t <= 2;
-    const int pa = card_closed ? 0 : (d - 2 - L) + 1;   // stage A: the phase after S_L is final
-    const int pb = pa + 1;                              // stage B (+ last tail level)
-    const int nS = d >= 2 ? d - 2 : 0, nW = L >= 1 ? L - 1 : 0;
+    const int pa = card_closed ? 0 : t - 2;   // stage A: the phase after S_L (scanned in phase t-3) is final
+    const int pb = pa + 1;                    // stage B (+ last tail level)
+    const int lastS = d >= 3 ? d - 3 : -1, lastW = L >= 2 ? L - 2 : -1;
     const int nfill = (T >= 2) ? 2 * (T - 1) : 0;
-    const int last = nS > nW ? (nS > pb + nfill ? nS : pb + nfill) : (nW > pb + nfill ? nW : pb + nfill);
-    const uint64_t CH = (top + gridDim.x - 1) / gridDim.x;
-    const uint64_t c0 = blockIdx.x * CH, c1 = (c0 + CH < top) ? c0 + CH : top;
+    int last = pb + nfill;
+    if (lastS > last) last = lastS;
+    if (lastW > last) last = lastW;
+    // column-scan CTAs of phase p (leading CTAs); the rest of the grid does the other work of p
+    auto ncols = [&](int p) -> uint64_t {
+        const int i = d - 3 - p, j = L - 2 - p;
+        uint64_t c = 0;
+        if (p >= 0 && i >= 0) c += G.g[i] < top ? G.g[i] : top;
+        if (p >= 0 && j >= 0) c += G.g[j] < top ? G.g[j] : top;
+        return c;
+    };
+    auto free0 = [&](int p) -> uint32_t {   // first CTA free of column scans in phase p (0: share the grid)
+        const uint64_t c = ncols(p);
+        return 2 * c <= gridDim.x ? (uint32_t)c : 0u;
+    };
+    // stage A / B chunks over the CTAs free in phase pb
+    const uint32_t b0 = free0(pb), nB = gridDim.x - b0;
+    const bool has_chunk = blockIdx.x >= b0;
+    const uint32_t cb = has_chunk ? blockIdx.x - b0 : 0;
+    const uint64_t CH = (top + nB - 1) / nB;
+    const uint64_t c0 = has_chunk ? (uint64_t)cb * CH : 0;
+    const uint64_t c1 = has_chunk ? ((c0 + CH < top) ? c0 + CH : top) : 0;
+    auto trace = [&](int p, int k) {   // diagnostics (FZ_K1_TRACE): per-CTA phase timestamps
+        if (tb.trace && threadIdx.x == 0 && p < 16) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            tb.trace[((uint64_t)blockIdx.x * 16 + p) * 2 + k] = t;
+        }
+    };
     for (int p = 0; p <= last; ++p) {
-        if (p > 0) grid_barrier(counter, target);
-        if (p == 0) {
+        if (p > 0) {
+            trace(p - 1, 1);
+            grid_barrier(counter, target);
+        }
+        trace(p, 0);
+        {   // column scans of S_{d-3-p} and W_{L-2-p}
+            const int i = d - 3 - p, j = L - 2 - p;
+            const uint64_t gi = i >= 0 ? G.g[i] : 1;
+            const uint64_t ncolS = i >= 0 ? (gi < top ? gi : top) : 0;
+            const uint64_t gj = j >= 0 ? G.g[j] : 1;
+            const uint64_t ncolW = j >= 0 ? (gj < top ? gj : top) : 0;
+            const uint64_t gw1 = L >= 1 ? G.g[L - 1] : 1;
+            for (uint64_t c = blockIdx.x; c < ncolS + ncolW; c += gridDim.x) {
+                if (c < ncolS) {
+                    uint64_t *dst = tb.S + (uint64_t)i * top;
+                    if (p == 0)
+                        block_column_scan_f([&](uint64_t x) { return prog_count(tb.P, (uint32_t)x); }, dst, top, gi,
+                                            c, sm);
+                    else
+                        block_column_scan(tb.S + (uint64_t)(i + 1) * top, dst, top, gi, c, sm);
+                } else {
+                    uint64_t *dst = tb.W + (uint64_t)j * top;
+                    if (p == 0)
+                        block_column_scan_f([&](uint64_t x) { return x / gw1 + 1; }, dst, top, gj, c - ncolS, sm);
+                    else
+                        block_column_scan(tb.W + (uint64_t)(j + 1) * top, dst, top, gj, c - ncolS, sm);
+                }
+            }
+        }
+        if (p == 0) {   // elementwise closed forms, from the last CTA down (the leading CTAs scan columns)
             const uint64_t gl = L > 0 ? G.g[L - 1] : 1;
-            for (uint64_t x = gt; x < top; x += ng) {
+            const uint64_t gtr = (gridDim.x - 1 - blockIdx.x) * (uint64_t)blockDim.x + threadIdx.x;
+            const uint64_t ng = (uint64_t)gridDim.x * blockDim.x;
+            for (uint64_t x = gtr; x < top; x += ng) {
                 tb.S[(uint64_t)d * top + x] = (x == 0) ? 1ull : 0ull;
                 tb.S[(uint64_t)(d - 1) * top + x] = (x % gd1 == 0) ? 1ull : 0ull;
                 if (d >= 2) tb.S[(uint64_t)(d - 2) * top + x] = prog_count(tb.P, (uint32_t)x);
                 tb.W[(uint64_t)L * top + x] = 1ull;
                 if (L > 0) tb.W[(uint64_t)(L - 1) * top + x] = x / gl + 1;
             }
-        } else {   // column scans of S_{d-2-p} and W_{L-1-p}
-            const int i = d - 2 - p, j = L - 1 - p;
-            const uint64_t gi = i >= 0 ? G.g[i] : 1;
-            const uint64_t ncolS = i >= 0 ? (gi < top ? gi : top) : 0;
-            const uint64_t gj = j >= 0 ? G.g[j] : 1;
-            const uint64_t ncolW = j >= 0 ? (gj < top ? gj : top) : 0;
-            for (uint64_t c = blockIdx.x; c < ncolS + ncolW; c += gridDim.x) {
-                if (c < ncolS)
-                    block_column_scan(tb.S + (uint64_t)(i + 1) * top, tb.S + (uint64_t)i * top, top, gi, c, sm);
-                else
-                    block_column_scan(tb.W + (uint64_t)(j + 1) * top, tb.W + (uint64_t)j * top, top, gj, c - ncolS,
-                                      sm);
-            }
         }
-        if (p == pa) {   // K2 stage A: chunk sums of card (memo rows only: x < ltop)
+        if (p == pa && has_chunk) {   // K2 stage A: chunk sums of card (memo rows only: x < ltop)
             uint64_t s = 0;
             for (uint64_t x = c0 + threadIdx.x; x < c1 && x < ltop; x += blockDim.x)
                 s += card_closed ? closed_card(x) : __ldcg(card + x);
             uint64_t tot;
             block_excl_scan(s, sm, &tot);
-            if (threadIdx.x == 0) tb.chunk[blockIdx.x] = tot;
+            if (threadIdx.x == 0) tb.chunk[cb] = tot;
         }
-        if (p == pb) {   // K2 stage B: off = exclusive scan of card; residue-major cardT / offT; last tail level
+        if (p == pb && has_chunk) {   // K2 stage B: off = exclusive scan of card; cardT / offT; last tail level
             uint64_t pre = 0;
-            for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += __ldcg(tb.chunk + b);
+            for (unsigned b = threadIdx.x; b < cb; b += blockDim.x) pre += __ldcg(tb.chunk + b);
             uint64_t tot;
             block_excl_scan(pre, sm, &tot);
             pre = tot;
@@ -866,13 +996,23 @@ __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigne
             if (p > pb && p <= pb + nfill) {
                 const int k = p - pb - 1, i = T - 2 - k / 2;
                 const uint32_t h = G.g[L + i];
-                if (k % 2 == 0)
-                    scan_a_body<T>(tb.S, tb.off, tb.rows, list, cap_list, top, ltop, L, i, h, gt >> 5, ng >> 5);
-                else
-                    scan_b_body<T>(tb.S, tb.off, tb.rows, list, cap_list, top, ltop, L, i, h, gt >> 5, ng >> 5);
+                const uint32_t f0 = free0(p);
+                if (blockIdx.x >= f0) {
+                    const uint64_t gt = (blockIdx.x - f0) * (uint64_t)blockDim.x + threadIdx.x;
+                    const uint64_t ng = (uint64_t)(gridDim.x - f0) * blockDim.x;
+                    const int lg = (k % 2 == 0) ? tb.lg_a[i] : tb.lg_b[i];
+                    const uint32_t lane = (uint32_t)threadIdx.x & ((1u << lg) - 1);
+                    if (k % 2 == 0)
+                        scan_a_body<T>(tb.S, tb.off, tb.rows, list, cap_list, top, ltop, L, i, h, gt >> lg, ng >> lg,
+                                       lane, 1u << lg);
+                    else
+                        scan_b_body<T>(tb.S, tb.off, tb.rows, list, cap_list, top, ltop, L, i, h, gt >> lg, ng >> lg,
+                                       lane, 1u << lg);
+                }
             }
         }
     }
+    trace(last, 1);
 }
 
 __global__ void __launch_bounds__(1024) k1_tables(Gens G, Tables tb, unsigned int *counter)
@@ -1223,9 +1363,6 @@ struct WalkTables {
     uint64_t R;              // rows per residue column
 };
 
-// x / g for x < 2^32 by the precomputed magic M = ceil(2^64 / g) (M = 0 encodes g = 1): the error of
-// x M / 2^64 against x / g is below x / 2^64 < 1 / g, so the floor is exact.
-__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint64_t M) { return M ? (uint32_t)__umul64hi(x, M) : x; }
 
 template <int D, int T, int MODE>
 __global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : 2)))
