@@ -210,38 +210,62 @@ __device__ __forceinline__ void grid_barrier(unsigned int *counter, unsigned int
 // Inclusive scan down one residue column c of a level:
 //   dst[x] = src(x) + dst[x - g]  for x = c, c+g, c+2g, ... < N.   One CTA.  src is a table in memory
 // or a closed form evaluated on the fly (the scans whose source level is closed run in phase 0).
+// One block barrier per round: warp w takes the contiguous rows [w S, (w+1) S) of the column
+// (S = ceil(rows / warps)), each lane E consecutive rows of them; warp-level scan, warp totals through
+// shared memory, and every warp adds the totals of the warps before it itself (no serial
+// second-level scan).  Columns longer than warps x 32 x kE rows take several rounds.
 template <class Src>
-__device__ void block_column_scan_f(Src src, uint64_t *dst, uint64_t N, uint64_t g, uint64_t c, uint64_t *sm)
+__device__ void block_column_scan_w(Src src, uint64_t *dst, uint64_t N, uint64_t g, uint64_t c, uint64_t *sm)
 {
-    constexpr int E = 8;
+    constexpr int kE = 4;
     const uint64_t rows = (N - c + g - 1) / g;
-    const uint64_t nt = blockDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint64_t per_round = (uint64_t)nwarps * 32 * kE;
     uint64_t carry = 0;
-    for (uint64_t k0 = 0; k0 < rows; k0 += nt * E) {
-        const uint64_t kb = k0 + threadIdx.x * (uint64_t)E;
-        uint64_t v[E];
+    for (uint64_t r0 = 0; r0 < rows; r0 += per_round) {
+        const uint64_t rr = (rows - r0 < per_round) ? rows - r0 : per_round;
+        const uint64_t S = (rr + nwarps - 1) / nwarps;           // rows per warp this round
+        const uint64_t ws = r0 + (uint64_t)warp * S;             // first row of this warp
+        const uint64_t we = (ws + S < r0 + rr) ? ws + S : r0 + rr;
+        const uint64_t kb = ws + (uint64_t)lane * kE;
+        uint64_t v[kE];
         uint64_t s = 0;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
+        for (int e = 0; e < kE; ++e) {
             const uint64_t k = kb + e;
-            v[e] = k < rows ? src(c + k * g) : 0;
+            v[e] = k < we ? src(c + k * g) : 0;
             s += v[e];
         }
-        uint64_t tot;
-        uint64_t run = carry + block_excl_scan(s, sm, &tot);
+        uint64_t inc = s;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t u = shfl_up_u64(inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) sm[warp] = inc;
+        __syncthreads();
+        uint64_t before = (lane < warp) ? sm[lane] : 0;   // totals of the warps before this one
+        uint64_t all = (lane < nwarps) ? sm[lane] : 0;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            before += __shfl_xor_sync(kFull, before, o);
+            all += __shfl_xor_sync(kFull, all, o);
+        }
+        uint64_t run = carry + before + inc - s;
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
             const uint64_t k = kb + e;
             run += v[e];
-            if (k < rows) dst[c + k * g] = run;
+            if (k < we) dst[c + k * g] = run;
         }
-        carry += tot;
+        carry += all;
+        __syncthreads();   // sm reused by the next round / the caller
     }
 }
 
 __device__ void block_column_scan(const uint64_t *src, uint64_t *dst, uint64_t N, uint64_t g, uint64_t c, uint64_t *sm)
 {
-    block_column_scan_f([=](uint64_t x) { return __ldcg(src + x); }, dst, N, g, c, sm);
+    block_column_scan_w([=](uint64_t x) { return __ldcg(src + x); }, dst, N, g, c, sm);
 }
 
 template <int T>
@@ -931,14 +955,14 @@ __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigne
                 if (c < ncolS) {
                     uint64_t *dst = tb.S + (uint64_t)i * top;
                     if (p == 0)
-                        block_column_scan_f([&](uint64_t x) { return prog_count(tb.P, (uint32_t)x); }, dst, top, gi,
+                        block_column_scan_w([&](uint64_t x) { return prog_count(tb.P, (uint32_t)x); }, dst, top, gi,
                                             c, sm);
                     else
                         block_column_scan(tb.S + (uint64_t)(i + 1) * top, dst, top, gi, c, sm);
                 } else {
                     uint64_t *dst = tb.W + (uint64_t)j * top;
                     if (p == 0)
-                        block_column_scan_f([&](uint64_t x) { return x / gw1 + 1; }, dst, top, gj, c - ncolS, sm);
+                        block_column_scan_w([&](uint64_t x) { return x / gw1 + 1; }, dst, top, gj, c - ncolS, sm);
                     else
                         block_column_scan(tb.W + (uint64_t)(j + 1) * top, dst, top, gj, c - ncolS, sm);
                 }
@@ -1361,6 +1385,7 @@ struct WalkTables {
     uint64_t gmag[kMaxD];    // division magic of each generator: x / g_j = umulhi64(x, gmag[j]) (+x if g_j = 1)
     uint32_t m;              // g_L (residue modulus of cardT / offT)
     uint64_t R;              // rows per residue column
+    uint32_t diag;           // diagnostics (FZ_K5_DIAG): bit 0 = MATERIALIZE without the output stores
 };
 
 
@@ -1639,7 +1664,10 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                         if (!ok[u]) continue;
                         const uint32_t q = q0 + 32 * u + lane;
                         if constexpr (MODE == FZ_MATERIALIZE) {
-                            store_row<D>(out + (outpos + q) * (uint64_t)D, wv[u]);
+                            if (wt.diag & 1u)
+                                acc_hash += wv[u][0] ^ wv[u][D - 1];   // keeps the row assembly alive
+                            else
+                                store_row<D>(out + (outpos + q) * (uint64_t)D, wv[u]);
                         } else {
                             acc_hash += row_hash<D>(row_base + outpos + q, wv[u]);
                         }
@@ -1683,7 +1711,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     }
     acc_rows = warp_sum_u64(acc_rows);
     if (lane == 0) atomicAdd((unsigned long long *)result, (unsigned long long)acc_rows);
-    if constexpr (MODE == FZ_HASH) {
+    if (MODE == FZ_HASH || (MODE == FZ_MATERIALIZE && (wt.diag & 1u))) {
         acc_hash = warp_sum_u64(acc_hash);
         if (lane == 0) atomicAdd((unsigned long long *)(result + 1), (unsigned long long)acc_hash);
     }
