@@ -1088,10 +1088,6 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
     const uint64_t gl = z.L > 0 ? m->lay->g[z.L - 1] : 1;
     a.wt.R = (z.top + gl - 1) / gl;
     a.wt.m = (uint32_t)gl;
-    {
-        const char *dg = getenv("FZ_K5_DIAG");   // diagnostics only (tools/quick_time.py experiments)
-        a.wt.diag = (dg && *dg) ? (uint32_t)atoi(dg) : 0u;
-    }
     for (int j = 0; j < FZ_MAX_D; ++j) {
         const uint64_t g = j < z.d ? m->lay->g[j] : 1;
         a.wt.gmag[j] = (g == 1) ? 0 : (~0ull / g + 1);   // ceil(2^64 / g)

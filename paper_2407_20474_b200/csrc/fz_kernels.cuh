@@ -1385,7 +1385,6 @@ struct WalkTables {
     uint64_t gmag[kMaxD];    // division magic of each generator: x / g_j = umulhi64(x, gmag[j]) (+x if g_j = 1)
     uint32_t m;              // g_L (residue modulus of cardT / offT)
     uint64_t R;              // rows per residue column
-    uint32_t diag;           // diagnostics (FZ_K5_DIAG): bit 0 = MATERIALIZE without the output stores
 };
 
 
@@ -1623,7 +1622,8 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 const unsigned nz = __ballot_sync(kFull, cc > 0);
                 if (cc > 0) {
                     const int e = __popc(nz & ((1u << lane) - 1));
-                    bi[e].memo_row = mrow;
+                    // byte address of the block's memo rows, pre-offset by its first output row (u64 wrap)
+                    bi[e].memo_row = (uint64_t)(uintptr_t)wt.memo + (mrow - excl) * (uint64_t)(4 * (T > 0 ? T : 1));
                     bi[e].start = excl;
                     bi[e].v = (uint32_t)vv;
                 }
@@ -1632,20 +1632,23 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 // UNR chunks of 32 rows are resolved and their memo tails loaded before any store,
                 // so each lane keeps UNR L2 loads in flight.
                 constexpr int UNR = (MODE == FZ_MATERIALIZE) ? 4 : 1;
-                int e0 = 0;
+                const uint32_t rel = cc > 0 ? excl : 0xffffffffu;   // this lane's block start (none: ~0)
+                uint32_t lm_le;                                       // lanes 0..lane
+                asm("mov.u32 %0, %%lanemask_le;" : "=r"(lm_le));
+                int before = -1;   // block starts before the chunk, minus one
                 for (uint32_t q0 = 0; q0 < use; q0 += 32 * UNR) {
                     uint32_t wv[UNR][D];
                     bool ok[UNR];
 #pragma unroll
                     for (int u = 0; u < UNR; ++u) {
                         const uint32_t qb = q0 + 32 * u;
-                        const unsigned bit = (cc > 0 && excl >= qb && excl - qb < 32) ? (1u << (excl - qb)) : 0u;
+                        uint32_t bit;   // 1 << (rel - qb), 0 unless the block starts inside this chunk
+                        asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(rel - qb));   // PTX clamps shifts >= 32 to 0
                         const unsigned M = __reduce_or_sync(kFull, bit);
-                        if (qb != 0) e0 += (int)(M & 1u);
                         const uint32_t q = qb + lane;
                         ok[u] = q < use;
-                        const int e = e0 + __popc(M & ((2u << lane) - 2u));
-                        e0 += __popc(M & 0xfffffffeu);
+                        const int e = before + __popc(M & lm_le);   // owner: the last block starting at or before q
+                        before += __popc(M);
                         if (ok[u]) {
                             const BlockInfo info = bi[e];
 #pragma unroll
@@ -1653,21 +1656,20 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                             wv[u][L - 1] = info.v;
                             if constexpr (T > 0) {
                                 uint32_t tw[T];
-                                load_tail<T>(wt.memo + (info.memo_row + (q - info.start)) * T, tw);
+                                load_tail<T>(reinterpret_cast<const uint32_t *>(info.memo_row + (uint64_t)q * (4 * T)),
+                                             tw);
 #pragma unroll
                                 for (int j = 0; j < T; ++j) wv[u][L + j] = tw[j];
                             }
                         }
                     }
+                    uint32_t *ob = out + (outpos + q0 + lane) * (uint64_t)D;   // chunk u at ob + 32 u D
 #pragma unroll
                     for (int u = 0; u < UNR; ++u) {
                         if (!ok[u]) continue;
                         const uint32_t q = q0 + 32 * u + lane;
                         if constexpr (MODE == FZ_MATERIALIZE) {
-                            if (wt.diag & 1u)
-                                acc_hash += wv[u][0] ^ wv[u][D - 1];   // keeps the row assembly alive
-                            else
-                                store_row<D>(out + (outpos + q) * (uint64_t)D, wv[u]);
+                            store_row<D>(ob + 32 * u * D, wv[u]);
                         } else {
                             acc_hash += row_hash<D>(row_base + outpos + q, wv[u]);
                         }
@@ -1711,7 +1713,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     }
     acc_rows = warp_sum_u64(acc_rows);
     if (lane == 0) atomicAdd((unsigned long long *)result, (unsigned long long)acc_rows);
-    if (MODE == FZ_HASH || (MODE == FZ_MATERIALIZE && (wt.diag & 1u))) {
+    if constexpr (MODE == FZ_HASH) {
         acc_hash = warp_sum_u64(acc_hash);
         if (lane == 0) atomicAdd((unsigned long long *)(result + 1), (unsigned long long)acc_hash);
     }
