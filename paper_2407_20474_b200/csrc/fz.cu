@@ -517,10 +517,9 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     const uint64_t f0 = a.n / a.G.g[0] + 1;
     const uint32_t f0n = (f0 <= 4096) ? (uint32_t)f0 : 0u;
     // COUNT: the residue-major card table as u16 in shared memory when its values and size allow
-    static const bool c16_env = [] {
-        const char *e = getenv("FZ_COUNT_SMEM");
-        return !(e && e[0] == '0');
-    }();
+    // FZ_COUNT_SMEM=0 never stages the table, =2 stages it whatever the walk size (tests)
+    const char *c16e = getenv("FZ_COUNT_SMEM");
+    const bool c16_env = !(c16e && c16e[0] == '0'), c16_force = c16e && c16e[0] == '2';
     // (x <= n, residue-major with R16 entries per column: a multiple of 8 with R16 / 8 odd, so the
     // 16-B vector loads of 8 lanes in different columns hit distinct banks), when the walk has enough
     // prefixes per CTA to repay the staging
@@ -530,7 +529,7 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     const uint32_t c16R = (MODE == FZ_COUNT && D - T >= 2 && c16_env && a.card_max < 65536 &&
                            a.card_max * (a.n / a.wt.m + 1) < (1ull << 32) &&   // per-lane u32 run sums
                            cbytes + f0n * 8 + 8 <= kCountSmemMax &&
-                           a.prefixes >= (a.n + 1) * 64 * (uint64_t)device_sms())
+                           (c16_force || a.prefixes >= (a.n + 1) * 64 * (uint64_t)device_sms()))
                               ? (uint32_t)R16
                               : 0u;
     const size_t smem = (size_t)(f0n + 1) / 2 * 16 + (c16R ? cbytes : 0);

@@ -1466,6 +1466,104 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
             // table staged in shared memory (u16, natural layout), whole runs go one per lane: lane l
             // takes sibling a_{L-2} - l and sums card[r_l - v m], v = 0..r_l / m, so the per-run
             // bookkeeping is shared by 32 runs.
+            if constexpr (L >= 3) {
+                if (c16R) {
+                    // Outer-prefix walk (staged card table, L >= 3): the slice [b, e) of leading-prefix
+                    // ranks takes exactly the outer prefixes (a_1..a_{L-2}) whose FIRST leading prefix has
+                    // its rank in [b, e) (every outer prefix in exactly one slice of one shard).  An outer
+                    // prefix with remainder R holds the runs a_{L-1} = A..0 (A = R / g_{L-1}), each the
+                    // innermost run v = rin / m .. 0 of remainder rin = R - a_{L-1} g_{L-1}; lane l sums
+                    // the runs A - l, A - l - 32, .. alone (one card lookup per leading prefix, no
+                    // per-run budget).  Ranks: the first leading prefix of an outer prefix has rank
+                    // sum_{j < L-2} W_j[r_j - (a_j + 1) g_j]; an outer prefix holds W_{L-2}[R] prefixes.
+                    const uint64_t b = shard_begin + sl.begin, e = b + sl.len;
+                    const uint32_t g2 = G.g[L - 2];
+                    const uint64_t mmag = wt.gmag[L - 1], g2mag = wt.gmag[L - 2];
+                    uint32_t o[L - 2], rj[L - 1];   // outer coordinates, remainders r_0 = n, r_{j+1}
+                    rj[0] = n;
+#pragma unroll
+                    for (int j = 0; j < L - 2; ++j) {
+                        o[j] = sl.a[j];
+                        rj[j + 1] = rj[j] - o[j] * G.g[j];
+                    }
+                    uint64_t ob = 0;
+#pragma unroll
+                    for (int j = 0; j < L - 2; ++j) {
+                        const uint32_t nx = (o[j] + 1) * G.g[j];
+                        if (nx <= rj[j]) ob += __ldg(Tb + (uint64_t)j * top + (rj[j] - nx));
+                    }
+                    const uint64_t *WL2 = Tb + (uint64_t)(L - 2) * top;
+                    // nextCandidate over the outer coordinates (rightmost nonzero a_i, i < L-2, decrements;
+                    // later outer coordinates restart at their maximum); false at the end of the stream
+                    auto outer_next = [&]() -> bool {
+                        int i = -1;
+#pragma unroll
+                        for (int j = 0; j < L - 2; ++j)
+                            if (o[j] > 0) i = j;
+                        if (i < 0) return false;
+#pragma unroll
+                        for (int j = 0; j < L - 2; ++j) {
+                            if (j == i) o[j] -= 1;
+                            if (j > i) o[j] = fdiv(rj[j], wt.gmag[j]);
+                            if (j >= i) rj[j + 1] = rj[j] - o[j] * G.g[j];
+                        }
+                        return true;
+                    };
+                    bool live = true;
+                    if (ob < b) {   // the outer prefix began in an earlier slice
+                        ob += __ldg(WL2 + rj[L - 2]);
+                        live = outer_next();
+                    }
+                    while (live && ob < e) {
+                        const uint32_t R = rj[L - 2];
+                        const uint32_t A = fdiv(R, g2mag);
+                        const uint32_t rmin = R - A * g2;
+                        for (uint32_t k = lane; k <= A; k += 32) {
+                            const uint32_t rl = rmin + k * g2;
+                            const uint32_t qq = fdiv(rl, mmag);
+                            const uint32_t len = qq + 1;
+                            const uint32_t cl = rl - qq * m;   // residue column; entries 0..len-1
+                            const uint4 *vp = reinterpret_cast<const uint4 *>(c16 + cl * c16R);
+                            const uint32_t nv = len >> 3;
+                            uint32_t s0 = 0, s1 = 0;
+                            uint32_t kk = 0;
+                            for (; kk + 2 <= nv; kk += 2) {
+                                const uint4 w0 = vp[kk], w1 = vp[kk + 1];
+                                s0 = __dp2a_lo(w0.x, 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.y, 0x0101u, s1);
+                                s0 = __dp2a_lo(w0.z, 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.w, 0x0101u, s1);
+                                s0 = __dp2a_lo(w1.x, 0x0101u, s0);
+                                s1 = __dp2a_lo(w1.y, 0x0101u, s1);
+                                s0 = __dp2a_lo(w1.z, 0x0101u, s0);
+                                s1 = __dp2a_lo(w1.w, 0x0101u, s1);
+                            }
+                            if (kk < nv) {   // odd full vector
+                                const uint4 w0 = vp[kk++];
+                                s0 = __dp2a_lo(w0.x, 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.y, 0x0101u, s1);
+                                s0 = __dp2a_lo(w0.z, 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.w, 0x0101u, s1);
+                            }
+                            const uint32_t tl = len & 7;   // last partial vector, masked
+                            if (tl) {
+                                const uint4 w0 = vp[kk];
+                                auto mk = [&](uint32_t i2) {
+                                    return tl > 2 * i2 + 1 ? 0xffffffffu : (tl > 2 * i2 ? 0xffffu : 0u);
+                                };
+                                s0 = __dp2a_lo(w0.x & mk(0), 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.y & mk(1), 0x0101u, s1);
+                                s0 = __dp2a_lo(w0.z & mk(2), 0x0101u, s0);
+                                s1 = __dp2a_lo(w0.w & mk(3), 0x0101u, s1);
+                            }
+                            acc_rows += s0 + s1;
+                        }
+                        ob += __ldg(WL2 + R);
+                        live = outer_next();
+                    }
+                    continue;
+                }
+            }
             uint32_t q = r_in / m, col = r_in - q * m;
             uint32_t vv = (uint32_t)v;
             uint32_t left32 = (uint32_t)left;   // K4 keeps COUNT slices below 2^31 prefixes

@@ -195,6 +195,21 @@ def test_c4_count(corc):
     assert tot == want
 
 
+@pytest.mark.parametrize("seed", range(32))
+def test_count_staged(seed, corc, monkeypatch):
+    """COUNT with the card table staged in shared memory, forced on small walks (FZ_COUNT_SMEM=2):
+    the outer-prefix walk (L >= 3) and the run-per-lane walk (L = 2) give the oracle's count, whole
+    and cut into 2, 3 and 7 shards, for every t."""
+    monkeypatch.setenv("FZ_COUNT_SMEM", "2")
+    for g, n in (random_instance(seed)[:2], random_instance_mid(seed)[:2]):
+        cnt = corc.gf_count(n, g)
+        for t in range(0, len(g)):
+            memo = fz.memo_build(g, t, n + 1, entries=False)
+            assert fz.enumerate(memo, n, "count")[1] == cnt, (g, n, t)
+            for k in (2, 3, 7):
+                assert sum(fz.enumerate(memo, n, "count", shard=s, nshards=k)[1] for s in range(k)) == cnt, (g, n, t, k)
+
+
 def test_c4_shape_hash(corc):
     """C4-shaped hash pin (n = 10000): 251 416 858 rows, H from SURVEY App. A."""
     memo = fz.memo_build(C4.gens, 3, 10001)
