@@ -1479,6 +1479,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                     const uint64_t b = shard_begin + sl.begin, e = b + sl.len;
                     const uint32_t g2 = G.g[L - 2];
                     const uint64_t mmag = wt.gmag[L - 1], g2mag = wt.gmag[L - 2];
+                    const uint32_t rdq = (uint32_t)((32ull * g2) / m), rdc = (uint32_t)((32ull * g2) % m);
                     uint32_t o[L - 2], rj[L - 1];   // outer coordinates, remainders r_0 = n, r_{j+1}
                     rj[0] = n;
 #pragma unroll
@@ -1518,45 +1519,55 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                         const uint32_t R = rj[L - 2];
                         const uint32_t A = fdiv(R, g2mag);
                         const uint32_t rmin = R - A * g2;
-                        for (uint32_t k = lane; k <= A; k += 32) {
-                            const uint32_t rl = rmin + k * g2;
-                            const uint32_t qq = fdiv(rl, mmag);
-                            const uint32_t len = qq + 1;
-                            const uint32_t cl = rl - qq * m;   // residue column; entries 0..len-1
-                            const uint4 *vp = reinterpret_cast<const uint4 *>(c16 + cl * c16R);
-                            const uint32_t nv = len >> 3;
-                            uint32_t s0 = 0, s1 = 0;
-                            uint32_t kk = 0;
-                            for (; kk + 2 <= nv; kk += 2) {
-                                const uint4 w0 = vp[kk], w1 = vp[kk + 1];
-                                s0 = __dp2a_lo(w0.x, 0x0101u, s0);
-                                s1 = __dp2a_lo(w0.y, 0x0101u, s1);
-                                s0 = __dp2a_lo(w0.z, 0x0101u, s0);
-                                s1 = __dp2a_lo(w0.w, 0x0101u, s1);
-                                s0 = __dp2a_lo(w1.x, 0x0101u, s0);
-                                s1 = __dp2a_lo(w1.y, 0x0101u, s1);
-                                s0 = __dp2a_lo(w1.z, 0x0101u, s0);
-                                s1 = __dp2a_lo(w1.w, 0x0101u, s1);
+                        if (lane <= A) {
+                            // run k = lane, lane + 32, ..: remainder rl = rmin + k g2, column rl mod m with
+                            // entries 0 .. rl / m; both stepped incrementally by 32 g2 = dq m + dc
+                            const uint32_t rl = rmin + lane * g2;
+                            uint32_t qq = fdiv(rl, mmag);
+                            uint32_t cl = rl - qq * m;
+                            for (uint32_t k = lane; k <= A; k += 32) {
+                                const uint32_t len = qq + 1;
+                                const uint4 *vp = reinterpret_cast<const uint4 *>(c16 + cl * c16R);
+                                const uint32_t nv = len >> 3;
+                                uint32_t s0 = 0, s1 = 0;
+                                uint32_t kk = 0;
+#pragma unroll 1
+                                for (; kk + 2 <= nv; kk += 2) {
+                                    const uint4 w0 = vp[kk], w1 = vp[kk + 1];
+                                    s0 = __dp2a_lo(w0.x, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w0.y, 0x0101u, s1);
+                                    s0 = __dp2a_lo(w0.z, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w0.w, 0x0101u, s1);
+                                    s0 = __dp2a_lo(w1.x, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w1.y, 0x0101u, s1);
+                                    s0 = __dp2a_lo(w1.z, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w1.w, 0x0101u, s1);
+                                }
+                                if (kk < nv) {   // odd full vector
+                                    const uint4 w0 = vp[kk++];
+                                    s0 = __dp2a_lo(w0.x, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w0.y, 0x0101u, s1);
+                                    s0 = __dp2a_lo(w0.z, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w0.w, 0x0101u, s1);
+                                }
+                                const uint32_t tl = len & 7;   // last partial vector: its first tl entries
+                                if (tl) {
+                                    const uint4 w0 = vp[kk];
+                                    const uint64_t mlo = tl >= 4 ? ~0ull : (1ull << (16 * tl)) - 1;
+                                    const uint64_t mhi = tl <= 4 ? 0ull : (1ull << (16 * (tl - 4))) - 1;
+                                    s0 = __dp2a_lo(w0.x & (uint32_t)mlo, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w0.y & (uint32_t)(mlo >> 32), 0x0101u, s1);
+                                    s0 = __dp2a_lo(w0.z & (uint32_t)mhi, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w0.w & (uint32_t)(mhi >> 32), 0x0101u, s1);
+                                }
+                                acc_rows += s0 + s1;
+                                cl += rdc;
+                                qq += rdq;
+                                if (cl >= m) {
+                                    cl -= m;
+                                    ++qq;
+                                }
                             }
-                            if (kk < nv) {   // odd full vector
-                                const uint4 w0 = vp[kk++];
-                                s0 = __dp2a_lo(w0.x, 0x0101u, s0);
-                                s1 = __dp2a_lo(w0.y, 0x0101u, s1);
-                                s0 = __dp2a_lo(w0.z, 0x0101u, s0);
-                                s1 = __dp2a_lo(w0.w, 0x0101u, s1);
-                            }
-                            const uint32_t tl = len & 7;   // last partial vector, masked
-                            if (tl) {
-                                const uint4 w0 = vp[kk];
-                                auto mk = [&](uint32_t i2) {
-                                    return tl > 2 * i2 + 1 ? 0xffffffffu : (tl > 2 * i2 ? 0xffffu : 0u);
-                                };
-                                s0 = __dp2a_lo(w0.x & mk(0), 0x0101u, s0);
-                                s1 = __dp2a_lo(w0.y & mk(1), 0x0101u, s1);
-                                s0 = __dp2a_lo(w0.z & mk(2), 0x0101u, s0);
-                                s1 = __dp2a_lo(w0.w & mk(3), 0x0101u, s1);
-                            }
-                            acc_rows += s0 + s1;
                         }
                         ob += __ldg(WL2 + R);
                         live = outer_next();
