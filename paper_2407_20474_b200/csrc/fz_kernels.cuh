@@ -1517,6 +1517,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                     }
                     while (live && ob < e) {
                         const uint32_t R = rj[L - 2];
+                        const uint64_t wR = __ldg(WL2 + R);   // prefixes of this outer prefix (used after the runs)
                         const uint32_t A = fdiv(R, g2mag);
                         const uint32_t rmin = R - A * g2;
                         if (lane <= A) {
@@ -1569,7 +1570,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                 }
                             }
                         }
-                        ob += __ldg(WL2 + R);
+                        ob += wR;
                         live = outer_next();
                     }
                     continue;
