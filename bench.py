@@ -4,8 +4,9 @@
 
 A step is one pass of the whole hot path over one element:
 memo build on the GPU (count pass K1 + copy-increment recurrence K3), device-side shard
-plan K4, enumeration K5 (materialize for C2, count for C4) and, for N > 1, the NCCL
-all-reduce of the {rows, hash} accumulators.  The A1 host layout (validation + sizing,
+plan K4, enumeration K5 (materialize for C2, count for C4) and, for N > 1 with one problem
+cut into shards (C4), the NCCL all-reduce of the {rows, hash} accumulators (A10); the weak C2
+batch has no data-path collective.  The A1 host layout (validation + sizing,
 like an FFT plan) is made once per configuration, outside the timed region.
 
 N = 1 runs BASELINE.json configs[1] (C2: Z(30232; 11,13,17,19), ~1e8 rows materialized).
@@ -138,8 +139,10 @@ def run_native(args, rank, world, local_rank):
         p.launch(out)                                                   # K5
         if ev_k5 is not None:
             ev_k5[1].record(stream)
-        if world > 1:
-            dist.all_reduce(p.result_tensor(), op=dist.ReduceOp.SUM)    # A10: {rows, hash}
+        if world > 1 and W["scaling"] == "strong":
+            # A10: {rows, hash} of the shards of ONE problem (the weak C2 batch has independent
+            # elements per rank: no data-path collective)
+            dist.all_reduce(p.result_tensor(), op=dist.ReduceOp.SUM)
         return m, p
 
     for _ in range(args.warmup):
@@ -148,8 +151,12 @@ def run_native(args, rank, world, local_rank):
     m0, p0 = step()
     torch.cuda.synchronize()
     r_step, h_step = p0.result()
-    if world == 1:
+    if world == 1 or W["scaling"] == "weak":
         assert r_step == rows_expect, (r_step, rows_expect)
+    if world > 1 and W["scaling"] == "weak":   # rows of the whole batch, once, outside the timed region
+        rt = torch.tensor([r_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(rt, op=dist.ReduceOp.SUM)
+        r_step = int(rt.item())
 
     k5_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                  for _ in range(args.steps)]
@@ -175,7 +182,7 @@ def run_native(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     ms_total = float(tt.item())
-    # r_step is the all-reduced {rows} accumulator for N > 1: every rank's rows of the step
+    # r_step: every rank's rows of the step (N > 1: the all-reduced shard accumulators, or the batch sum)
     rows_per_step = float(r_step)
     value = rows_per_step * args.steps / (ms_total / 1e3)
     r_local = rows_expect
@@ -233,7 +240,9 @@ def run_native(args, rank, world, local_rank):
         "clocks": sampler.summary(),
     }
     if world > 1:
-        res["config"]["collective"] = "NCCL all_reduce(SUM) of the {rows, hash} accumulators each step"
+        res["config"]["collective"] = ("NCCL all_reduce(SUM) of the {rows, hash} shard accumulators each step"
+                                       if W["scaling"] == "strong" else
+                                       "none in the data path (independent elements per rank)")
     return res, (g, n, t, mode)
 
 
