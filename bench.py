@@ -280,6 +280,47 @@ def count_mode_extra(local_rank):
     return res
 
 
+def hash_mode_extra(local_rank):
+    """Hash mode on BASELINE.json configs[2] (C3: Z(17350; 23,29,31,37,41,43), 1.0e10 rows, t = 3 — the
+    fastest memo dimension): whole step (memo build + plan + the HASH walk), CUDA-event timed; the
+    (count, H) pair is compared with the known answer in tests/golden/hash_kats.csv."""
+    import torch
+
+    from fzinputs import C3_GENS, C3_N
+    from paper_2407_20474_b200 import fz
+
+    g, n, t, steps = C3_GENS, C3_N, 3, 3
+    kat = None
+    for line in open(os.path.join(ROOT, "tests", "golden", "hash_kats.csv")):
+        f = line.strip().split(",")
+        if len(f) >= 4 and f[0] == ";".join(map(str, g)) and f[1] == str(n):
+            kat = (int(f[2]), int(f[3], 16))
+    lay = fz.Layout(g, t, n + 1, entries=True)
+    ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device="cuda")
+    pws = None
+
+    def step():
+        nonlocal pws
+        m = fz.Memo(layout=lay, workspace=ws)
+        if pws is None:
+            pws = torch.empty(fz.plan_workspace_bytes(m), dtype=torch.uint8, device="cuda")
+        p = fz.Plan(m, n, "hash", workspace=pws)
+        p.launch()
+        return m, p
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    keep = [step() for _ in range(steps)]
+    e1.record()
+    torch.cuda.synchronize()
+    rows, h = keep[-1][1].result()
+    ms = e0.elapsed_time(e1) / steps
+    return {"C3": {"value": rows / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "rows": rows, "t": t,
+                   "hash": f"{h:#018x}", "kat_match": kat == (rows, h),
+                   "workload": f"Z({n}; {','.join(map(str, g))}) hash, t={t}"}}
+
+
 def run_e2e(args, spec, W, rank, world, local_rank):
     """Same metric end to end through the public API from HOST buffers, on every rank; the timed region
     (barrier-bracketed, max over ranks) holds each step's H2D of the generator tuple and D2H of the result.
@@ -475,6 +516,7 @@ def main():
             res["cpu_baseline"] = cpu_baseline(spec)
         if world == 1 and args.config == "C2" and not args.no_count:
             res["count_mode"] = count_mode_extra(local_rank)
+            res["hash_mode"] = hash_mode_extra(local_rank)
         print(json.dumps(res), flush=True)
     if world > 1:
         dist.barrier()
