@@ -1405,7 +1405,14 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
         for (uint32_t x = threadIdx.x; x <= (uint32_t)n64; x += blockDim.x)
             c16[(x % mm) * c16R + x / mm] = (uint16_t)__ldg(wt.card64 + x);
     }
-    if (f0n || c16R) __syncthreads();
+    // COUNT: masks keeping the first tl u16 entries of a 16-B vector, tl = 0..7
+    __shared__ uint4 tailmask[MODE == FZ_COUNT ? 8 : 1];
+    if (MODE == FZ_COUNT && threadIdx.x < 8) {
+        const uint32_t tl = threadIdx.x;
+        auto w = [&](uint32_t i) { return tl > 2 * i + 1 ? 0xffffffffu : (tl > 2 * i ? 0xffffu : 0u); };
+        tailmask[MODE == FZ_COUNT ? tl : 0] = make_uint4(w(0), w(1), w(2), w(3));
+    }
+    __syncthreads();
     constexpr int L = D - T;
     static_assert(L >= 1, "at least one leading coordinate");
     __shared__ BlockInfo binfo[MODE == FZ_COUNT ? 1 : kWalkThreads / 32][32];   // MAT/HASH block lists
@@ -1553,13 +1560,11 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                 }
                                 const uint32_t tl = len & 7;   // last partial vector: its first tl entries
                                 if (tl) {
-                                    const uint4 w0 = vp[kk];
-                                    const uint64_t mlo = tl >= 4 ? ~0ull : (1ull << (16 * tl)) - 1;
-                                    const uint64_t mhi = tl <= 4 ? 0ull : (1ull << (16 * (tl - 4))) - 1;
-                                    s0 = __dp2a_lo(w0.x & (uint32_t)mlo, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w0.y & (uint32_t)(mlo >> 32), 0x0101u, s1);
-                                    s0 = __dp2a_lo(w0.z & (uint32_t)mhi, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w0.w & (uint32_t)(mhi >> 32), 0x0101u, s1);
+                                    const uint4 w0 = vp[kk], mk = tailmask[tl];
+                                    s0 = __dp2a_lo(w0.x & mk.x, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w0.y & mk.y, 0x0101u, s1);
+                                    s0 = __dp2a_lo(w0.z & mk.z, 0x0101u, s0);
+                                    s1 = __dp2a_lo(w0.w & mk.w, 0x0101u, s1);
                                 }
                                 acc_rows += s0 + s1;
                                 cl += rdc;
