@@ -27,4 +27,13 @@ for fill in (0, 1, 2, 3, 4, 5):
             ok = ok and fz.enumerate(memo, n, "count")[1] == cnt
             bad += (not ok)
 fz.set_fill_mode(0)
+# staged COUNT walks forced on small instances: the outer-prefix walk (L >= 3) and the run-per-lane walk (L = 2)
+os.environ["FZ_COUNT_SMEM"] = "2"
+for g, n, t in [((13, 37, 38, 40, 41), 600, 1), ((3, 5, 8, 11), 200, 1), ((3, 5, 8, 11), 200, 2),
+                ((13, 37, 38, 40, 41), 600, 2)]:
+    memo = fz.memo_build(g, t, n + 1, entries=False)
+    cnt = C.gf_count(n, g)
+    for ns in (1, 3):
+        bad += sum(fz.enumerate(memo, n, "count", shard=s, nshards=ns)[1] for s in range(ns)) != cnt
+os.environ["FZ_COUNT_SMEM"] = ""
 print("sanitize subset:", "OK" if bad == 0 else f"{bad} FAILURES")
