@@ -1746,7 +1746,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 // flattened copy: rows q0 + lane of the round, owner block via block-start bitmask.
                 // UNR chunks of 32 rows are resolved and their memo tails loaded before any store,
                 // so each lane keeps UNR L2 loads in flight.
-                constexpr int UNR = (MODE == FZ_MATERIALIZE) ? 4 : 1;
+                constexpr int UNR = (MODE == FZ_MATERIALIZE) ? 4 : 2;
                 const uint32_t rel = cc > 0 ? excl : 0xffffffffu;   // this lane's block start (none: ~0)
                 uint32_t lm_le;                                       // lanes 0..lane
                 asm("mov.u32 %0, %%lanemask_le;" : "=r"(lm_le));
