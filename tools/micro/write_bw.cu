@@ -14,6 +14,42 @@ __global__ void copy(const uint4 *__restrict__ a, uint4 *b, size_t n)
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
+// K5's store pattern: each warp owns one contiguous region (a slice) and writes it front to back in
+// batches of 4 x 512 B (4 chunks of 32 rows x 16 B), with `slices` regions taken in order by a queue
+__global__ void region_fill(uint4 *p, size_t n, size_t per_slice, size_t slices, unsigned long long *queue, uint32_t v)
+{
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long s = 0;
+        if (lane == 0) s = atomicAdd(queue, 1ull);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= slices) break;
+        const size_t b = s * per_slice, e = (b + per_slice < n) ? b + per_slice : n;
+        for (size_t i = b + lane; i < e; i += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + 32 * u < e)
+                    asm volatile("st.global.cs.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p + i + 32 * u), "r"(v) : "memory");
+        }
+    }
+}
+
+// the same with static round-robin slices (warp w takes slices w, w + nw, ...): no queue atomics
+__global__ void region_fill_static(uint4 *p, size_t n, size_t per_slice, size_t slices, uint32_t v)
+{
+    const int lane = threadIdx.x & 31;
+    const size_t w = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5, nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+    for (size_t s = w; s < slices; s += nw) {
+        const size_t b = s * per_slice, e = (b + per_slice < n) ? b + per_slice : n;
+        for (size_t i = b + lane; i < e; i += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + 32 * u < e)
+                    asm volatile("st.global.cs.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p + i + 32 * u), "r"(v) : "memory");
+        }
+    }
+}
+
 int main()
 {
     const size_t bytes = 1600010896ull & ~15ull, n = bytes / 16;
@@ -34,6 +70,39 @@ int main()
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         printf("fill 1.6 GB, %2d CTAs/SM x 256: %.1f us  %.0f GB/s\n", bpsm, ms * 100, bytes / (ms / 10 / 1e3) / 1e9);
+    }
+    {
+        unsigned long long *queue;
+        cudaMalloc(&queue, 8);
+        for (size_t slices : {(size_t)75759, (size_t)4736, (size_t)sms * 4 * 8 * 64}) {
+            const size_t per = (n + slices - 1) / slices;
+            for (int it = 0; it < 3; ++it) {
+                cudaMemset(queue, 0, 8);
+                region_fill<<<sms * 4, 256>>>(p, n, per, slices, queue, it);
+            }
+            float tot = 0;
+            for (int it = 0; it < 10; ++it) {
+                cudaMemset(queue, 0, 8);
+                cudaEventRecord(e0);
+                region_fill<<<sms * 4, 256>>>(p, n, per, slices, queue, it);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                tot += ms;
+            }
+            printf("region fill 1.6 GB, %zu slices (warp-owned, 2 KB batches), 4 CTAs/SM x 256: %.1f us  %.0f GB/s\n",
+                   slices, tot * 100, bytes / (tot / 10 / 1e3) / 1e9);
+            for (int it = 0; it < 3; ++it) region_fill_static<<<sms * 4, 256>>>(p, n, per, slices, it);
+            cudaEventRecord(e0);
+            for (int it = 0; it < 10; ++it) region_fill_static<<<sms * 4, 256>>>(p, n, per, slices, it);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms2;
+            cudaEventElapsedTime(&ms2, e0, e1);
+            printf("region fill 1.6 GB, %zu slices, static round-robin, 4 CTAs/SM x 256: %.1f us  %.0f GB/s\n", slices,
+                   ms2 * 100, bytes / (ms2 / 10 / 1e3) / 1e9);
+        }
     }
     for (int it = 0; it < 3; ++it) copy<<<sms * 8, 256>>>(p, q, n);
     cudaEventRecord(e0);
