@@ -523,9 +523,12 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     // (x <= n, residue-major with R16 entries per column: a multiple of 8 with R16 / 8 odd, so the
     // 16-B vector loads of 8 lanes in different columns hit distinct banks), when the walk has enough
     // prefixes per CTA to repay the staging
-    uint64_t R16 = (a.n / a.wt.m + 1 + 7) / 8 * 8;
-    if ((R16 / 8) % 2 == 0) R16 += 8;
-    const uint64_t cbytes = R16 * a.wt.m * 2;
+    // u8 entries (16 per vector, R16 / 16 odd) when every card < 256 and the outer-prefix walk runs (L >= 3)
+    const bool u8 = MODE == FZ_COUNT && D - T >= 3 && a.card_max < 256;
+    const uint64_t per_vec = u8 ? 16 : 8;
+    uint64_t R16 = (a.n / a.wt.m + 1 + per_vec - 1) / per_vec * per_vec;
+    if ((R16 / per_vec) % 2 == 0) R16 += per_vec;
+    const uint64_t cbytes = R16 * a.wt.m * (u8 ? 1 : 2);
     const uint32_t c16R = (MODE == FZ_COUNT && D - T >= 2 && c16_env && a.card_max < 65536 &&
                            a.card_max * (a.n / a.wt.m + 1) < (1ull << 32) &&   // per-lane u32 run sums
                            cbytes + f0n * 8 + 8 <= kCountSmemMax &&
@@ -548,7 +551,7 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
         last_smem = smem;
     }
     fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::walk_threads<MODE>(), smem, s>>>(
-        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n, c16R);
+        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n, c16R, (uint32_t)(u8 && c16R));
     ++g_launches;
     return cuda_check("k5_walk");
 }

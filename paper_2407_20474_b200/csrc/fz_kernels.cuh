@@ -23,6 +23,7 @@
 //                       store instruction writes 32 consecutive rows.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "../../include/fz.h"
@@ -1393,23 +1394,38 @@ __global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : 
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
-                                                         uint32_t f0n, uint32_t c16R)
+                                                         uint32_t f0n, uint32_t c16R, uint32_t c8)
 {
     extern __shared__ uint64_t f0s[];   // level-0 unrank column (f0n entries, 0 = not cached)
     for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Tb + (n64 - (uint64_t)q * G.g[0]));
-    // COUNT: card[x] = S_L[x], x <= n, as u16 in shared memory after f0s, residue-major w.r.t. m = g_L with
-    // c16R entries per residue column (16-B aligned columns; c16R = 0: not staged)
+    // COUNT: card[x] = S_L[x], x <= n, in shared memory after f0s, residue-major w.r.t. m = g_L with c16R
+    // entries per residue column (16-B aligned columns; c16R = 0: not staged); u16 entries, or u8 when c8
+    // (every card < 256, outer-prefix walk only)
     uint16_t *c16 = reinterpret_cast<uint16_t *>(f0s + ((f0n + 1) & ~1u));
+    uint8_t *c8t = reinterpret_cast<uint8_t *>(c16);
     if (c16R) {
         const uint32_t mm = G.g[D - T - 1];
-        for (uint32_t x = threadIdx.x; x <= (uint32_t)n64; x += blockDim.x)
-            c16[(x % mm) * c16R + x / mm] = (uint16_t)__ldg(wt.card64 + x);
+        for (uint32_t x = threadIdx.x; x <= (uint32_t)n64; x += blockDim.x) {
+            const uint32_t i = (x % mm) * c16R + x / mm;
+            const uint64_t c = __ldg(wt.card64 + x);
+            if (c8)
+                c8t[i] = (uint8_t)c;
+            else
+                c16[i] = (uint16_t)c;
+        }
     }
-    // COUNT: masks keeping the first tl u16 entries of a 16-B vector, tl = 0..7
-    __shared__ uint4 tailmask[MODE == FZ_COUNT ? 8 : 1];
-    if (MODE == FZ_COUNT && threadIdx.x < 8) {
+    // COUNT: masks keeping the first tl entries of a 16-B vector (tl = 0..7 u16 entries, 0..15 u8 entries)
+    __shared__ uint4 tailmask[MODE == FZ_COUNT ? 16 : 1];
+    if (MODE == FZ_COUNT && threadIdx.x < 16) {
         const uint32_t tl = threadIdx.x;
-        auto w = [&](uint32_t i) { return tl > 2 * i + 1 ? 0xffffffffu : (tl > 2 * i ? 0xffffu : 0u); };
+        auto w = [&](uint32_t i) {   // word i of the mask
+            if (c8) {
+                uint32_t r = 0;
+                for (uint32_t b = 0; b < 4; ++b) r |= (4 * i + b < tl) ? 0xffu << (8 * b) : 0u;
+                return r;
+            }
+            return tl > 2 * i + 1 ? 0xffffffffu : (tl > 2 * i ? 0xffffu : 0u);
+        };
         tailmask[MODE == FZ_COUNT ? tl : 0] = make_uint4(w(0), w(1), w(2), w(3));
     }
     __syncthreads();
@@ -1533,38 +1549,73 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                             const uint32_t rl = rmin + lane * g2;
                             uint32_t qq = fdiv(rl, mmag);
                             uint32_t cl = rl - qq * m;
+                            auto runs = [&](auto u8tag) {   // the run loop, compiled once per card width
+                            constexpr bool kU8 = decltype(u8tag)::value;
                             for (uint32_t k = lane; k <= A; k += 32) {
                                 const uint32_t len = qq + 1;
-                                const uint4 *vp = reinterpret_cast<const uint4 *>(c16 + cl * c16R);
-                                const uint32_t nv = len >> 3;
                                 uint32_t s0 = 0, s1 = 0;
-                                uint32_t kk = 0;
+                                if constexpr (kU8) {   // u8 cards: 16 per vector, 4 per dp4a
+                                    const uint4 *vp = reinterpret_cast<const uint4 *>(c8t + cl * c16R);
+                                    const uint32_t nv = len >> 4;
+                                    uint32_t kk = 0;
 #pragma unroll 1
-                                for (; kk + 2 <= nv; kk += 2) {
-                                    const uint4 w0 = vp[kk], w1 = vp[kk + 1];
-                                    s0 = __dp2a_lo(w0.x, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w0.y, 0x0101u, s1);
-                                    s0 = __dp2a_lo(w0.z, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w0.w, 0x0101u, s1);
-                                    s0 = __dp2a_lo(w1.x, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w1.y, 0x0101u, s1);
-                                    s0 = __dp2a_lo(w1.z, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w1.w, 0x0101u, s1);
-                                }
-                                if (kk < nv) {   // odd full vector
-                                    const uint4 w0 = vp[kk++];
-                                    s0 = __dp2a_lo(w0.x, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w0.y, 0x0101u, s1);
-                                    s0 = __dp2a_lo(w0.z, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w0.w, 0x0101u, s1);
-                                }
-                                const uint32_t tl = len & 7;   // last partial vector: its first tl entries
-                                if (tl) {
-                                    const uint4 w0 = vp[kk], mk = tailmask[tl];
-                                    s0 = __dp2a_lo(w0.x & mk.x, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w0.y & mk.y, 0x0101u, s1);
-                                    s0 = __dp2a_lo(w0.z & mk.z, 0x0101u, s0);
-                                    s1 = __dp2a_lo(w0.w & mk.w, 0x0101u, s1);
+                                    for (; kk + 2 <= nv; kk += 2) {
+                                        const uint4 w0 = vp[kk], w1 = vp[kk + 1];
+                                        s0 = __dp4a(w0.x, 0x01010101u, s0);
+                                        s1 = __dp4a(w0.y, 0x01010101u, s1);
+                                        s0 = __dp4a(w0.z, 0x01010101u, s0);
+                                        s1 = __dp4a(w0.w, 0x01010101u, s1);
+                                        s0 = __dp4a(w1.x, 0x01010101u, s0);
+                                        s1 = __dp4a(w1.y, 0x01010101u, s1);
+                                        s0 = __dp4a(w1.z, 0x01010101u, s0);
+                                        s1 = __dp4a(w1.w, 0x01010101u, s1);
+                                    }
+                                    if (kk < nv) {   // odd full vector
+                                        const uint4 w0 = vp[kk++];
+                                        s0 = __dp4a(w0.x, 0x01010101u, s0);
+                                        s1 = __dp4a(w0.y, 0x01010101u, s1);
+                                        s0 = __dp4a(w0.z, 0x01010101u, s0);
+                                        s1 = __dp4a(w0.w, 0x01010101u, s1);
+                                    }
+                                    const uint32_t tl = len & 15;   // last partial vector: its first tl entries
+                                    if (tl) {
+                                        const uint4 w0 = vp[kk], mk = tailmask[tl];
+                                        s0 = __dp4a(w0.x & mk.x, 0x01010101u, s0);
+                                        s1 = __dp4a(w0.y & mk.y, 0x01010101u, s1);
+                                        s0 = __dp4a(w0.z & mk.z, 0x01010101u, s0);
+                                        s1 = __dp4a(w0.w & mk.w, 0x01010101u, s1);
+                                    }
+                                } else {
+                                    const uint4 *vp = reinterpret_cast<const uint4 *>(c16 + cl * c16R);
+                                    const uint32_t nv = len >> 3;
+                                    uint32_t kk = 0;
+#pragma unroll 1
+                                    for (; kk + 2 <= nv; kk += 2) {
+                                        const uint4 w0 = vp[kk], w1 = vp[kk + 1];
+                                        s0 = __dp2a_lo(w0.x, 0x0101u, s0);
+                                        s1 = __dp2a_lo(w0.y, 0x0101u, s1);
+                                        s0 = __dp2a_lo(w0.z, 0x0101u, s0);
+                                        s1 = __dp2a_lo(w0.w, 0x0101u, s1);
+                                        s0 = __dp2a_lo(w1.x, 0x0101u, s0);
+                                        s1 = __dp2a_lo(w1.y, 0x0101u, s1);
+                                        s0 = __dp2a_lo(w1.z, 0x0101u, s0);
+                                        s1 = __dp2a_lo(w1.w, 0x0101u, s1);
+                                    }
+                                    if (kk < nv) {   // odd full vector
+                                        const uint4 w0 = vp[kk++];
+                                        s0 = __dp2a_lo(w0.x, 0x0101u, s0);
+                                        s1 = __dp2a_lo(w0.y, 0x0101u, s1);
+                                        s0 = __dp2a_lo(w0.z, 0x0101u, s0);
+                                        s1 = __dp2a_lo(w0.w, 0x0101u, s1);
+                                    }
+                                    const uint32_t tl = len & 7;   // last partial vector: its first tl entries
+                                    if (tl) {
+                                        const uint4 w0 = vp[kk], mk = tailmask[tl];
+                                        s0 = __dp2a_lo(w0.x & mk.x, 0x0101u, s0);
+                                        s1 = __dp2a_lo(w0.y & mk.y, 0x0101u, s1);
+                                        s0 = __dp2a_lo(w0.z & mk.z, 0x0101u, s0);
+                                        s1 = __dp2a_lo(w0.w & mk.w, 0x0101u, s1);
+                                    }
                                 }
                                 acc_rows += s0 + s1;
                                 cl += rdc;
@@ -1574,6 +1625,11 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                     ++qq;
                                 }
                             }
+                            };
+                            if (c8)
+                                runs(std::true_type{});
+                            else
+                                runs(std::false_type{});
                         }
                         ob += wR;
                         live = outer_next();
