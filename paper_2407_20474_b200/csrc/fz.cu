@@ -12,6 +12,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/fz.h"
@@ -46,6 +47,29 @@ fz_status cuda_check(const char *what)
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(FZ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
     return FZ_OK;
+}
+
+// Programmatic dependent launch (PDL): the kernel may be scheduled while the previous kernel of the
+// stream drains; it calls griddepcontrol.wait before reading anything that kernel wrote.
+// FZ_PDL=0 launches plainly (A/B comparisons).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args)
+{
+    static const bool on = [] {
+        const char *e = getenv("FZ_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = on ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 #define FZ_CUDA(call)                                                                   \
@@ -550,8 +574,9 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
         per_sm = std::min(per_sm, 8);
         last_smem = smem;
     }
-    fzk::k5_walk<D, T, MODE><<<(unsigned)(device_sms() * per_sm), fzk::walk_threads<MODE>(), smem, s>>>(
-        a.G, a.n, a.hdr, a.Tb, a.top, a.wt, a.out, a.cap, a.row_base, f0n, c16R, (uint32_t)(u8 && c16R));
+    FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE>, dim3((unsigned)(device_sms() * per_sm)),
+                       dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
+                       a.wt, a.out, (uint64_t)a.cap, (uint64_t)a.row_base, f0n, c16R, (uint32_t)(u8 && c16R)));
     ++g_launches;
     return cuda_check("k5_walk");
 }
@@ -1041,7 +1066,12 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
     A.nshards = nshards;
     A.L = z.L;
     Gens G = make_gens(m->lay->g, z.d);
-    fzk::k4_plan<<<1, 32, 0, (cudaStream_t)stream>>>(G, A, m->S, m->W, (PlanHdr *)p->d_plan);
+    const cudaError_t le = launch_pdl(fzk::k4_plan, dim3(1), dim3(32), 0, (cudaStream_t)stream, G, A,
+                                      (const uint64_t *)m->S, (const uint64_t *)m->W, (PlanHdr *)p->d_plan);
+    if (le != cudaSuccess) {
+        delete p;
+        return fail(FZ_ECUDA, "k4_plan launch: %s", cudaGetErrorString(le));
+    }
     ++g_launches;
     fz_status st = cuda_check("k4_plan");
     if (st) {

@@ -277,6 +277,11 @@ __device__ __forceinline__ void incr_word(uint32_t (&w)[T], int i)
 }
 
 // ------------------------------------------------------------ PTX helpers
+// Programmatic dependent launch: wait for the preceding kernel of the stream (no-op without PDL).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// ... and let the next kernel of the stream be scheduled now (it still waits for this one's completion).
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
@@ -945,6 +950,7 @@ __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigne
             grid_barrier(counter, target);
         }
         trace(p, 0);
+        if (p == last) griddep_launch();   // PDL: the planner may be scheduled during the last phase
         {   // column scans of S_{d-3-p} and W_{L-2-p}
             const int i = d - 3 - p, j = L - 2 - p;
             const uint64_t gi = i >= 0 ? G.g[i] : 1;
@@ -1265,6 +1271,8 @@ __device__ uint64_t row_rank(const uint64_t *__restrict__ S, uint64_t top, const
 __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t *__restrict__ S,
                                                const uint64_t *__restrict__ W, PlanHdr *hdr)
 {
+    griddep_wait();   // PDL: the count tables of the memo build are complete and visible
+    griddep_launch();
     const int lane = threadIdx.x & 31;
     const bool count_mode = (A.mode == FZ_COUNT) && A.L > 0;   // t = d (L = 0): rows in every mode
     const uint64_t *Tb = count_mode ? W : S;
@@ -1396,6 +1404,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
                                                          uint32_t f0n, uint32_t c16R, uint32_t c8)
 {
+    griddep_wait();   // PDL: the plan header (K4) and the memo tables are complete and visible
     extern __shared__ uint64_t f0s[];   // level-0 unrank column (f0n entries, 0 = not cached)
     for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Tb + (n64 - (uint64_t)q * G.g[0]));
     // COUNT: card[x] = S_L[x], x <= n, in shared memory after f0s, residue-major w.r.t. m = g_L with c16R
