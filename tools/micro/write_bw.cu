@@ -50,6 +50,42 @@ __global__ void region_fill_static(uint4 *p, size_t n, size_t per_slice, size_t 
     }
 }
 
+// store-cache-hint variants of the static region fill: 0 = .cs (K5), 1 = default (.wb), 2 = .L2::evict_last-free
+template <int V>
+__global__ void region_fill_v(uint4 *p, size_t n, size_t per_slice, size_t slices, uint32_t v)
+{
+    const int lane = threadIdx.x & 31;
+    const size_t w = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5, nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+    for (size_t s = w; s < slices; s += nw) {
+        const size_t b = s * per_slice, e = (b + per_slice < n) ? b + per_slice : n;
+        for (size_t i = b + lane; i < e; i += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + 32 * u < e) {
+                    if (V == 0)
+                        asm volatile("st.global.cs.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p + i + 32 * u), "r"(v) : "memory");
+                    else if (V == 1)
+                        asm volatile("st.global.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p + i + 32 * u), "r"(v) : "memory");
+                    else
+                        asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p + i + 32 * u), "r"(v) : "memory");
+                }
+        }
+    }
+}
+
+template <int V>
+float time_v(uint4 *p, size_t n, size_t per, size_t slices, int grid, cudaEvent_t e0, cudaEvent_t e1)
+{
+    for (int it = 0; it < 3; ++it) region_fill_v<V><<<grid, 256>>>(p, n, per, slices, it);
+    cudaEventRecord(e0);
+    for (int it = 0; it < 10; ++it) region_fill_v<V><<<grid, 256>>>(p, n, per, slices, it);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms / 10;
+}
+
 int main()
 {
     const size_t bytes = 1600010896ull & ~15ull, n = bytes / 16;
@@ -103,6 +139,13 @@ int main()
             printf("region fill 1.6 GB, %zu slices, static round-robin, 4 CTAs/SM x 256: %.1f us  %.0f GB/s\n", slices,
                    ms2 * 100, bytes / (ms2 / 10 / 1e3) / 1e9);
         }
+    }
+    for (int bpsm : {4, 8}) {
+        const size_t slices = 75759, per = (n + slices - 1) / slices;
+        const float a = time_v<0>(p, n, per, slices, sms * bpsm, e0, e1), b = time_v<1>(p, n, per, slices, sms * bpsm, e0, e1),
+                    c = time_v<2>(p, n, per, slices, sms * bpsm, e0, e1);
+        printf("region fill (75759 static slices, %d CTAs/SM): st.cs %.1f us, st (wb) %.1f us, st.L1::no_allocate %.1f us\n",
+               bpsm, a * 1e3, b * 1e3, c * 1e3);
     }
     for (int it = 0; it < 3; ++it) copy<<<sms * 8, 256>>>(p, q, n);
     cudaEventRecord(e0);
