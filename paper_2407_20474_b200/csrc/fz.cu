@@ -564,9 +564,13 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     static thread_local size_t last_smem = ~(size_t)0;
     static thread_local int per_sm = 0;
     if (smem != last_smem) {
-        if (smem > 48 * 1024)
+        if (smem > 48 * 1024) {
             FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
+            if constexpr (MODE == FZ_COUNT && D - T >= 3)
+                FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        }
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::walk_threads<MODE>(),
                                                           std::max<size_t>(smem, 4096 * 8)) != cudaSuccess ||
             per_sm < 1)
@@ -574,9 +578,19 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
         per_sm = std::min(per_sm, 8);
         last_smem = smem;
     }
-    FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE>, dim3((unsigned)(device_sms() * per_sm)),
-                       dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
-                       a.wt, a.out, (uint64_t)a.cap, (uint64_t)a.row_base, f0n, c16R, (uint32_t)(u8 && c16R)));
+    auto go = [&](auto kern) {
+        return launch_pdl(kern, dim3((unsigned)(device_sms() * per_sm)), dim3(fzk::walk_threads<MODE>()), smem, s, a.G,
+                          (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top, a.wt, a.out, (uint64_t)a.cap,
+                          (uint64_t)a.row_base, f0n, c16R);
+    };
+    if constexpr (MODE == FZ_COUNT && D - T >= 3) {
+        if (u8 && c16R)
+            FZ_CUDA(go(fzk::k5_walk<D, T, MODE, true>));
+        else
+            FZ_CUDA(go(fzk::k5_walk<D, T, MODE, false>));
+    } else {
+        FZ_CUDA(go(fzk::k5_walk<D, T, MODE, false>));
+    }
     ++g_launches;
     return cuda_check("k5_walk");
 }

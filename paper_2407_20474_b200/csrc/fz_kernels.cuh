@@ -23,7 +23,6 @@
 //                       store instruction writes 32 consecutive rows.
 #pragma once
 #include <cstdint>
-#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "../../include/fz.h"
@@ -1397,13 +1396,14 @@ struct WalkTables {
 };
 
 
-template <int D, int T, int MODE>
+template <int D, int T, int MODE, bool U8 = false>
 __global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : 2)))
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
-                                                         uint32_t f0n, uint32_t c16R, uint32_t c8)
+                                                         uint32_t f0n, uint32_t c16R)
 {
+    constexpr bool c8 = U8;   // COUNT outer-prefix walk with u8 cards (every card < 256)
     griddep_wait();   // PDL: the plan header (K4) and the memo tables are complete and visible
     extern __shared__ uint64_t f0s[];   // level-0 unrank column (f0n entries, 0 = not cached)
     for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Tb + (n64 - (uint64_t)q * G.g[0]));
@@ -1558,12 +1558,10 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                             const uint32_t rl = rmin + lane * g2;
                             uint32_t qq = fdiv(rl, mmag);
                             uint32_t cl = rl - qq * m;
-                            auto runs = [&](auto u8tag) {   // the run loop, compiled once per card width
-                            constexpr bool kU8 = decltype(u8tag)::value;
                             for (uint32_t k = lane; k <= A; k += 32) {
                                 const uint32_t len = qq + 1;
                                 uint32_t s0 = 0, s1 = 0;
-                                if constexpr (kU8) {   // u8 cards: 16 per vector, 4 per dp4a
+                                if constexpr (U8) {   // u8 cards: 16 per vector, 4 per dp4a
                                     const uint4 *vp = reinterpret_cast<const uint4 *>(c8t + cl * c16R);
                                     const uint32_t nv = len >> 4;
                                     uint32_t kk = 0;
@@ -1634,11 +1632,6 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                     ++qq;
                                 }
                             }
-                            };
-                            if (c8)
-                                runs(std::true_type{});
-                            else
-                                runs(std::false_type{});
                         }
                         ob += wR;
                         live = outer_next();
