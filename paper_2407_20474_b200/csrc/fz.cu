@@ -410,10 +410,12 @@ fzk::ProgGens make_prog(const uint32_t *g, int d)
 
 constexpr uint64_t kPlanHeader = 256;
 
-uint64_t max_slices()
+// K5 queue granularity: slices per resident warp (measured optimum: 16 for MATERIALIZE / HASH, whose
+// slices are row ranges; 64 for COUNT, whose outer prefixes vary more in work)
+uint64_t max_slices(fz_mode mode)
 {
     static const char *e = getenv("FZ_SLICES_PER_WARP");
-    const uint64_t per_warp = (e && atoi(e) > 0) ? (uint64_t)atoi(e) : 16;
+    const uint64_t per_warp = (e && atoi(e) > 0) ? (uint64_t)atoi(e) : (mode == FZ_COUNT ? 64 : 16);
     return (uint64_t)device_sms() * 4 * (fzk::kWalkThreads / 32) * per_warp;
 }
 
@@ -1073,7 +1075,7 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
     PlanArgs A;
     A.n = n;
     A.top = z.top;
-    A.max_slices = max_slices();
+    A.max_slices = max_slices(mode);
     A.floor_len = (mode == FZ_COUNT) ? 1024 : 32;
     A.mode = (int)mode;
     A.shard = shard;
