@@ -1,4 +1,5 @@
 // Microbenchmark: cost of the K1 grid barrier and of one column scan phase on B200.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/micro/grid_barrier tools/micro/grid_barrier.cu
 #include <cstdio>
 #include <cstdint>
 #include <vector>

@@ -1,4 +1,5 @@
 // Microbenchmark: achievable HBM write bandwidth on this B200 for a pure 16-B streaming-store fill
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/micro/write_bw tools/micro/write_bw.cu
 // (the roofline ceiling of K5 materialize), and a copy for comparison.
 #include <cstdio>
 #include <cstdint>
