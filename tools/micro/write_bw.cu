@@ -87,6 +87,41 @@ float time_v(uint4 *p, size_t n, size_t per, size_t slices, int grid, cudaEvent_
     return ms / 10;
 }
 
+// K5's pattern with a non-persistent grid: CTA b takes the contiguous slice range [b S / nb, (b+1) S / nb),
+// its warps round-robin inside it; more CTAs than resident ones (several waves, like the grid-stride fill)
+__global__ void region_fill_waves(uint4 *p, size_t n, size_t per_slice, size_t slices, uint32_t v)
+{
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const size_t s0 = slices * blockIdx.x / gridDim.x, s1 = slices * (blockIdx.x + 1) / gridDim.x;
+    for (size_t s = s0 + wib; s < s1; s += nwb) {
+        const size_t b = s * per_slice, e = (b + per_slice < n) ? b + per_slice : n;
+        for (size_t i = b + lane; i < e; i += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + 32 * u < e)
+                    asm volatile("st.global.cs.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p + i + 32 * u), "r"(v) : "memory");
+        }
+    }
+}
+
+// the same address order with persistent CTAs: CTA b runs the virtual CTAs v = b, b + grid, .. (V of them)
+__global__ void region_fill_virtual(uint4 *p, size_t n, size_t per_slice, size_t slices, size_t V, uint32_t v)
+{
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    for (size_t vb = blockIdx.x; vb < V; vb += gridDim.x) {
+        const size_t s0 = slices * vb / V, s1 = slices * (vb + 1) / V;
+        for (size_t s = s0 + wib; s < s1; s += nwb) {
+            const size_t b = s * per_slice, e = (b + per_slice < n) ? b + per_slice : n;
+            for (size_t i = b + lane; i < e; i += 128) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (i + 32 * u < e)
+                        asm volatile("st.global.cs.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p + i + 32 * u), "r"(v) : "memory");
+            }
+        }
+    }
+}
+
 int main()
 {
     const size_t bytes = 1600010896ull & ~15ull, n = bytes / 16;
@@ -147,6 +182,32 @@ int main()
                     c = time_v<2>(p, n, per, slices, sms * bpsm, e0, e1);
         printf("region fill (75759 static slices, %d CTAs/SM): st.cs %.1f us, st (wb) %.1f us, st.L1::no_allocate %.1f us\n",
                bpsm, a * 1e3, b * 1e3, c * 1e3);
+    }
+    for (int waves : {1, 2, 4, 8}) {
+        const size_t slices = 75759, per = (n + slices - 1) / slices;
+        const int grid = sms * 4 * waves;
+        for (int it = 0; it < 3; ++it) region_fill_waves<<<grid, 256>>>(p, n, per, slices, it);
+        cudaEventRecord(e0);
+        for (int it = 0; it < 10; ++it) region_fill_waves<<<grid, 256>>>(p, n, per, slices, it);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("region fill, 75759 slices in per-CTA contiguous ranges, %d x 4 CTAs/SM (4 resident): %.1f us\n", waves,
+               ms * 100);
+    }
+    for (int waves : {1, 4, 8, 16}) {
+        const size_t slices = 75759, per = (n + slices - 1) / slices;
+        const int grid = sms * 4;
+        const size_t V = (size_t)grid * waves;
+        for (int it = 0; it < 3; ++it) region_fill_virtual<<<grid, 256>>>(p, n, per, slices, V, it);
+        cudaEventRecord(e0);
+        for (int it = 0; it < 10; ++it) region_fill_virtual<<<grid, 256>>>(p, n, per, slices, V, it);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("region fill, persistent 4 CTAs/SM running %d x virtual CTAs in order: %.1f us\n", waves, ms * 100);
     }
     for (int it = 0; it < 3; ++it) copy<<<sms * 8, 256>>>(p, q, n);
     cudaEventRecord(e0);
