@@ -13,6 +13,11 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    # the suites load libfz.so / liboracle.so: (re)build them when missing or older than their sources
+    # (nvcc cross-compiles sm_100a without a GPU; a no-op when both are up to date)
+    import __graft_entry__
+
+    __graft_entry__.build()
 
 
 def read_golden_csv(name):
