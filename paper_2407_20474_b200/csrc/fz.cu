@@ -726,6 +726,68 @@ void host_unrank_prefix(const fz_layout *lay, uint64_t n, uint64_t R, uint32_t *
 
 uint64_t mul_div_h(uint64_t U, uint64_t a, uint64_t b) { return (U / b) * a + ((U % b) * a) / b; }
 
+// COUNT shard cut balanced by cost instead of leading prefixes: a prefix costs 1 (its card lookup) and each
+// innermost run (a_1..a_{L-1} fixed) costs beta more (its per-run bookkeeping in the walk), i.e. the table
+// C_j = W_j + beta V_j (V_j counts the runs; the same column-scan recurrence as W). Shard s starts at the
+// leading prefix holding cost rank C_0[n] s / k; its W-rank is the unit boundary K4 uses. Any boundary is
+// an exact cover, so the cut only moves work between shards. FZ_COUNT_RUN_COST sets beta (0: plain cut).
+uint64_t count_cut(const fz_layout *lay, uint64_t n, int nshards, int s)
+{
+    const uint64_t P = lay->H.W[n];
+    static const uint64_t beta = [] {
+        const char *e = getenv("FZ_COUNT_RUN_COST");
+        return (e && *e) ? (uint64_t)strtoull(e, nullptr, 10) : (uint64_t)32;
+    }();
+    const int L = lay->z.L;
+    if (s <= 0) return 0;
+    if (s >= nshards) return P;
+    if (beta == 0 || L < 2) return mul_div_h(P, (uint64_t)s, (uint64_t)nshards);
+    const uint64_t top = n + 1;
+    // C_{L}[x] = 1 (one lookup), C_{L-1}[x] = x / g_{L-1} + 1 + beta, C_j = column scan of C_{j+1} by g_j;
+    // cached per thread for the last (layout, n) (a plan per step must not rebuild it)
+    static thread_local uint32_t c_g[FZ_MAX_D];
+    static thread_local int c_L = -1, c_d = -1;
+    static thread_local uint64_t c_n = ~0ull;
+    static thread_local std::vector<uint64_t> C;
+    bool hit = c_L == L && c_d == lay->z.d && c_n == n;
+    for (int j = 0; hit && j < lay->z.d; ++j) hit = c_g[j] == lay->g[j];
+    if (!hit) {
+        C.assign((size_t)(L + 1) * top, 0);
+        for (uint64_t x = 0; x < top; ++x) {
+            C[(size_t)L * top + x] = 1;
+            C[(size_t)(L - 1) * top + x] = x / lay->g[L - 1] + 1 + beta;
+        }
+        for (int j = L - 2; j >= 0; --j) {
+            const uint64_t gj = lay->g[j];
+            uint64_t *Cj = C.data() + (size_t)j * top;
+            const uint64_t *Cn = Cj + top;
+            for (uint64_t x = 0; x < top; ++x) Cj[x] = Cn[x] + (x >= gj ? Cj[x - gj] : 0);
+        }
+        for (int j = 0; j < lay->z.d; ++j) c_g[j] = lay->g[j];
+        c_L = L;
+        c_d = lay->z.d;
+        c_n = n;
+    }
+    const uint64_t total = C[n];
+    uint64_t R = mul_div_h(total, (uint64_t)s, (uint64_t)nshards);
+    // unrank the cost rank R (descending lex, as host_unrank_prefix) and take that prefix's W-rank
+    uint64_t r = n, wrank = 0;
+    for (int j = 0; j < L; ++j) {
+        const uint64_t gj = lay->g[j], amax = r / gj;
+        // cumulative cost of the candidates a_j = amax .. a+1: sum_{a' > a} Tj[r - a' gj] = C_j[r - (a+1) gj]
+        const uint64_t *Cj = C.data() + (size_t)j * top;
+        uint64_t lo = 0, hi = amax;   // largest a with C_j[r - a gj] > R
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo + 1) / 2;
+            if (Cj[r - mid * gj] > R) lo = mid; else hi = mid - 1;
+        }
+        R -= (lo + 1 <= amax) ? Cj[r - (lo + 1) * gj] : 0;   // (at j = L-1, C carries the run's beta: last level)
+        if (lo + 1 <= amax) wrank += lay->H.W[(size_t)j * lay->z.top + (r - (lo + 1) * gj)];
+        r -= lo * gj;
+    }
+    return wrank < P ? wrank : P;
+}
+
 // same shard cut as k4_plan, on the host tables
 void host_shard(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, int s, uint64_t &rb, uint64_t &rl)
 {
@@ -738,8 +800,8 @@ void host_shard(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, int
             host_unrank_prefix(lay, n, pidx, a);
             return host_row_rank(lay, n, a);
         };
-        rb = rowat(mul_div_h(P, s, nshards));
-        rl = rowat(mul_div_h(P, s + 1, nshards)) - rb;
+        rb = rowat(count_cut(lay, n, nshards, s));
+        rl = rowat(count_cut(lay, n, nshards, s + 1)) - rb;
     } else {
         rb = mul_div_h(rows_total, s, nshards);
         rl = mul_div_h(rows_total, s + 1, nshards) - rb;
@@ -1081,6 +1143,13 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
     A.shard = shard;
     A.nshards = nshards;
     A.L = z.L;
+    A.cut_given = 0;
+    A.ub = A.ue = 0;
+    if (mode == FZ_COUNT && z.L > 0 && nshards > 1) {   // cost-balanced COUNT cut (host tables)
+        A.cut_given = 1;
+        A.ub = count_cut(m->lay, n, nshards, shard);
+        A.ue = count_cut(m->lay, n, nshards, shard + 1);
+    }
     Gens G = make_gens(m->lay->g, z.d);
     const cudaError_t le = launch_pdl(fzk::k4_plan, dim3(1), dim3(32), 0, (cudaStream_t)stream, G, A,
                                       (const uint64_t *)m->S, (const uint64_t *)m->W, (PlanHdr *)p->d_plan);

@@ -69,6 +69,8 @@ struct PlanArgs {
     uint64_t max_slices;
     uint64_t floor_len;
     int mode, shard, nshards, L;
+    int cut_given;       // COUNT: the shard's unit range [ub, ue) comes from the host's cost-balanced cut
+    uint64_t ub, ue;
 };
 
 // x / g for x < 2^32 by the precomputed magic M = ceil(2^64 / g) (M = 0 encodes g = 1): the error of
@@ -1276,7 +1278,8 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
     const bool count_mode = (A.mode == FZ_COUNT) && A.L > 0;   // t = d (L = 0): rows in every mode
     const uint64_t *Tb = count_mode ? W : S;
     const uint64_t U = __ldg(Tb + A.n);
-    const uint64_t ub = mul_div(U, A.shard, A.nshards), ue = mul_div(U, A.shard + 1, A.nshards);
+    const uint64_t ub = A.cut_given ? A.ub : mul_div(U, A.shard, A.nshards);
+    const uint64_t ue = A.cut_given ? A.ue : mul_div(U, A.shard + 1, A.nshards);
     const uint64_t len = ue - ub;
     uint64_t slice_len = (len + A.max_slices - 1) / A.max_slices;
     if (slice_len < A.floor_len) slice_len = A.floor_len;
