@@ -206,7 +206,8 @@ def run_native(args, rank, world, local_rank):
         # of the card table; bound: the shared-memory crossbar, 128 B/clk/SM (B300_MICROARCH.md, LDS/STS)
         # -> SMs x 128 / 2 lookups per clock at the max SM clock
         U = leading_prefixes(g, n, len(g) - t)
-        units = U * (W["shard"] + 1) // W["nshards"] - U * W["shard"] // W["nshards"]
+        # N > 1: the COUNT shards are cost-balanced, not unit-balanced; U / N is their mean
+        units = U // W["nshards"]
         props = torch.cuda.get_device_properties(dev)
         clk = sampler.summary().get("sm_max_mhz") or 1965
         peak = props.multi_processor_count * 128 / 2 * clk * 1e6
@@ -214,6 +215,8 @@ def run_native(args, rank, world, local_rank):
                 "unit": "card lookups/s (leading prefixes)", "peak": peak,
                 "peak_source": "derived: SMs x 128 B/clk shared-memory crossbar / 2 B per u16 card x max SM clock",
                 "algorithmic_units_per_launch": units, "frac": units / (k5_ms / 1e3) / peak}
+        if W["nshards"] > 1:
+            roof["units_note"] = "mean units per shard (cost-balanced COUNT cut)"
     roof["traffic"] = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "k5_traffic.json")))
