@@ -1476,7 +1476,11 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
         sl.len = (shard_len - sl.begin) < slice_len ? (shard_len - sl.begin) : slice_len;
         {
             uint32_t ua[kMaxD];
-            const uint64_t k0 = unrank(Tb, top, G, L, n64, shard_begin + sl.begin, ua, f0n ? f0s : nullptr);
+#pragma unroll
+            for (int j = 0; j < kMaxD; ++j) ua[j] = 0;
+            // the COUNT outer-prefix walk needs only the outer prefix (a_1..a_{L-2}) holding the slice start
+            const int ulev = (MODE == FZ_COUNT && L >= 3 && c16R) ? L - 2 : L;
+            const uint64_t k0 = unrank(Tb, top, G, ulev, n64, shard_begin + sl.begin, ua, f0n ? f0s : nullptr);
             sl.k0 = (MODE == FZ_COUNT) ? 0 : k0;
 #pragma unroll
             for (int j = 0; j < L; ++j) sl.a[j] = ua[j];
