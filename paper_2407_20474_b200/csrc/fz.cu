@@ -1137,7 +1137,9 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
     PlanArgs A;
     A.n = n;
     A.top = z.top;
-    A.max_slices = max_slices(mode);
+    // COUNT shards of a 4-way or wider cut take half the slices (each shard re-pays the slice starts;
+    // measured: 8 shards 0.71 -> 0.74 of linear, one shard 1 % slower)
+    A.max_slices = max_slices(mode) / ((mode == FZ_COUNT && nshards >= 4) ? 2 : 1);
     A.floor_len = (mode == FZ_COUNT) ? 1024 : 32;
     A.mode = (int)mode;
     A.shard = shard;
