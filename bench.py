@@ -2,27 +2,35 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--config C2|C4]
 
-A step is one pass of the whole hot path over one element:
-memo build on the GPU (count pass K1 + copy-increment recurrence K3), device-side shard
-plan K4, enumeration K5 (materialize for C2, count for C4) and, for N > 1 with one problem
-cut into shards (C4), the NCCL all-reduce of the {rows, hash} accumulators (A10); the weak C2
-batch has no data-path collective.  The A1 host layout (validation + sizing,
-like an FFT plan) is made once per configuration, outside the timed region.
+A step is one pass of the whole hot path over one problem: memo build on the
+GPU (count pass K1 + copy-increment recurrence K3), device-side shard plan K4, enumeration K5 and, when
+one problem is cut into shards over N > 1 ranks, the NCCL all_reduce of the {rows, hash} accumulators
+(A10).  The A1 host layout (validation + sizing, like an FFT plan) is made once per configuration,
+outside the timed region.
 
-N = 1 runs BASELINE.json configs[1] (C2: Z(30232; 11,13,17,19), ~1e8 rows materialized).
-For N > 1 (torchrun, one process per GPU) C2 is a batch of N independent elements, one per
-GPU (n_r = 30232 - r): per-GPU work fixed -> "scaling": "weak"; --config C4 instead splits
-ONE count problem (Z(40000; 97..104), 3.36e12 rows) across the ranks -> "strong".
+Headline workload:
+  N = 1: BASELINE.json configs[1] (C2: Z(30232; 11,13,17,19), 100 000 681 rows materialized).
+  N > 1: ONE count problem cut into N shards (C4: Z(40000; 97..104), t = 3, 3.36e12 rows; BASELINE
+         configs[3], the north-star multi-GPU target) -> "scaling": "strong".  The same line carries the
+         other legs as extra keys ("legs"): C2 materialize row-sharded (strong) and the C2 batch of N
+         independent elements (weak), so each workload can be compared across N.
+  --config C4 (or C2) forces the headline workload at any N.
+At N = 1 the line also carries count_mode (C2, C4 t=3) and hash_mode (C3 t=3) legs, each with a roofline.
 
-`--impl reference` times the CPU oracle (oracle/, the plain nested-loop definition) on this
-host's cores on a bounded sample of the same workload (there is no reference program to
-install: the reference is a paper).
+`python bench.py --gpus N` without torchrun spawns the N ranks itself (torch.distributed.run, one process
+per GPU, NCCL); with fewer visible GPUs than N the ranks share them over gloo, and the line says so.
+
+`--impl reference` times the CPU oracle (oracle/, the plain nested-loop definition) on this host's cores
+on a bounded sample of the same workload (there is no reference program to install: the reference is a
+paper).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -41,16 +49,23 @@ def _env_int(k, d):
         return d
 
 
-def workload(cfg: str, rank: int, world: int):
+def workload(name: str, rank: int, world: int):
+    """The bench workloads (fixed tuples from fzinputs, BASELINE.json configs)."""
     from fzinputs import C2, C4
 
-    if cfg == "C2":
-        return dict(name="C2", gens=C2.gens, n=C2.n - rank, t=C2.t, mode="materialize", shard=0, nshards=1,
+    if name == "C2":        # configs[1]: one element materialized (N = 1), or row-sharded over the ranks
+        return dict(name="C2", gens=C2.gens, n=C2.n, t=C2.t, mode="materialize", shard=rank, nshards=world,
+                    scaling="strong" if world > 1 else "weak")
+    if name == "C2batch":   # N independent elements, one per rank (n_r = 30232 - r)
+        return dict(name="C2batch", gens=C2.gens, n=C2.n - rank, t=C2.t, mode="materialize", shard=0, nshards=1,
                     scaling="weak")
-    if cfg == "C4":
+    if name == "C4":        # configs[3]: one count problem cut into N shards
         return dict(name="C4", gens=C4.gens, n=C4.n, t=C4.t, mode="count", shard=rank, nshards=world,
                     scaling="strong")
-    raise SystemExit(f"unknown --config {cfg}")
+    if name == "C4t2":
+        return dict(name="C4t2", gens=C4.gens, n=C4.n, t=2, mode="count", shard=rank, nshards=world,
+                    scaling="strong")
+    raise SystemExit(f"unknown workload {name}")
 
 
 # ------------------------------------------------------------------ clocks (NVML)
@@ -110,244 +125,281 @@ class ClockSampler:
                 "samples": len(s)}
 
 
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def _profile_counters():
+    """Per-launch counters captured once with ncu (profiles/k5_counters.json): DRAM bytes and warp
+    instructions of each leg's dominant kernel at the current kernel version."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "k5_counters.json")))
+    except Exception:
+        return {}
+
+
+def leading_prefixes(g, n: int, L: int) -> int:
+    """Leading prefixes (a_1..a_L) with phi <= n = sum_{x<=n} |Z(x; g_1..g_L)| (coin-change counts;
+    measurement bookkeeping for the COUNT roofline, not part of the product path)."""
+    import numpy as np
+
+    c = np.zeros(n + 1, dtype=np.int64)
+    c[0] = 1
+    for gi in g[:L]:
+        for r in range(min(gi, n + 1)):
+            c[r::gi] = np.cumsum(c[r::gi])
+    return int(c.sum())
+
+
+def roofline(W, plan, k5_ms: float, rows_local: int, sm_max_mhz, props, world: int):
+    """Roofline of the leg's dominant kernel (K5): algorithmic units per launch / its CUDA-event time.
+    MATERIALIZE: HBM bytes written (4 d per row).  COUNT: card lookups (one per leading prefix, SURVEY
+    §8(d)) against the shared-memory crossbar, 128 B/clk/SM (B300_MICROARCH.md LDS/STS) / bytes per card.
+    HASH: issue slots -- the kernel's ncu warp-instruction count (profiles/k5_counters.json) against
+    SMs x 4 SMSPs x 1 instr/clk."""
+    g, n, t, mode = W["gens"], W["n"], W["t"], W["mode"]
+    d = len(g)
+    peaks = _peaks()
+    clk = (sm_max_mhz or peaks.get("sm_max_mhz") or 1965) * 1e6
+    sms = props.multi_processor_count
+    walk, card_bytes = plan.walk()
+    counters = _profile_counters().get(W["name"], {})
+    if mode == "materialize":
+        alg = rows_local * d * 4
+        peak = peaks.get("hbm_gbs")
+        r = {"kernel": f"k5_walk<{d},{t},materialize>", "bound": "hbm", "achieved": alg / (k5_ms / 1e3) / 1e9,
+             "peak": peak if peak else 6650.0,
+             "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md)",
+             "unit": "GB/s", "algorithmic_bytes_per_launch": alg,
+             "derivation": "4 d bytes per output row (one 16-B store per row at d = 4) / K5 event time"}
+    elif mode == "count":
+        U = leading_prefixes(g, n, d - t)
+        units = U / W["nshards"]
+        peak = sms * 128 / card_bytes * clk
+        r = {"kernel": f"k5_pairs<{d},{t},{'u8' if card_bytes == 1 else 'u16'}>" if walk == "count_pairs"
+             else f"k5_walk<{d},{t},count>", "bound": "smem",
+             "achieved": units / (k5_ms / 1e3), "peak": peak, "unit": "card lookups/s",
+             "peak_source": (f"derived: {sms} SMs x 128 B/clk shared-memory crossbar (B300_MICROARCH.md LDS/STS) / "
+                             f"{card_bytes} B per card x {clk / 1e6:.0f} MHz"),
+             "algorithmic_units_per_launch": units,
+             "derivation": "one card lookup per leading prefix (a_1..a_{d-t}), SURVEY §8(d); / K5 event time"}
+        if W["nshards"] > 1:
+            r["units_note"] = "mean lookups per shard (the cut balances modelled cost, not lookups)"
+    else:
+        inst = counters.get("warp_inst_per_launch")
+        peak = sms * 4 * clk
+        r = {"kernel": f"k5_walk<{d},{t},hash>", "bound": "issue", "unit": "warp instructions/s", "peak": peak,
+             "peak_source": f"derived: {sms} SMs x 4 SMSPs x 1 warp instruction/clk x {clk / 1e6:.0f} MHz",
+             "achieved": (inst / (k5_ms / 1e3)) if inst else None,
+             "algorithmic_units_per_launch": inst,
+             "derivation": ("warp instructions per launch from ncu (smsp__inst_executed.sum, "
+                            "profiles/k5_counters.json) / K5 event time")}
+    r["frac"] = (r["achieved"] / r["peak"]) if r.get("achieved") else None
+    r["traffic"] = counters.get("dram_bytes_per_launch")
+    r["k5_ms"] = k5_ms
+    r["walk"] = walk
+    return r
+
+
 # ------------------------------------------------------------------ native arm
-def run_native(args, rank, world, local_rank):
+def measure(W, steps: int, warmup: int, rank: int, world: int, dev, sampler=None):
+    """Time `steps` whole steps of workload W on this rank (barrier + synchronize on both sides, CUDA
+    events on the launching stream, max over ranks).  Returns a dict."""
     import torch
     import torch.distributed as dist
 
     from paper_2407_20474_b200 import fz
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    W = workload(args.config, rank, world)
     g, n, t, mode = W["gens"], W["n"], W["t"], W["mode"]
-    entries = mode != "count"
-    lay = fz.Layout(g, t, n + 1, entries=entries)                  # A1 (host, once)
+    lay = fz.Layout(g, t, n + 1, entries=mode != "count")          # A1 (host, once)
     ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device=dev)
     memo = fz.Memo(layout=lay, workspace=ws)
     pws = torch.empty(fz.plan_workspace_bytes(memo), dtype=torch.uint8, device=dev)
     plan = fz.Plan(memo, n, mode, W["shard"], W["nshards"], workspace=pws)
-    rows_expect = plan.rows
-    out = torch.empty((max(rows_expect, 1), len(g)), dtype=torch.int32, device=dev) if mode == "materialize" else None
+    rows_local = plan.rows
+    out = (torch.empty((max(rows_local, 1), len(g)), dtype=torch.int32, device=dev)
+           if mode == "materialize" else None)
     stream = torch.cuda.current_stream()
+    collective = world > 1 and W["scaling"] == "strong"
 
-    def step(ev_k5=None):
-        m = fz.Memo(layout=lay, workspace=ws)                          # K1 + K3
-        p = fz.Plan(m, n, mode, W["shard"], W["nshards"], workspace=pws)   # K4
-        if ev_k5 is not None:
-            ev_k5[0].record(stream)
-        p.launch(out)                                                   # K5
-        if ev_k5 is not None:
-            ev_k5[1].record(stream)
-        if world > 1 and W["scaling"] == "strong":
-            # A10: {rows, hash} of the shards of ONE problem (the weak C2 batch has independent
-            # elements per rank: no data-path collective)
+    def step(ev=None):
+        m = fz.Memo(layout=lay, workspace=ws)                               # K1 + K3
+        p = fz.Plan(m, n, mode, W["shard"], W["nshards"], workspace=pws)    # K4
+        if ev is not None:
+            ev[0].record(stream)
+        p.launch(out)                                                       # K5
+        if ev is not None:
+            ev[1].record(stream)
+        if collective:   # A10: {rows, hash} of the shards of ONE problem, NCCL, straight from the plan header
             dist.all_reduce(p.result_tensor(), op=dist.ReduceOp.SUM)
         return m, p
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     m0, p0 = step()
     torch.cuda.synchronize()
     r_step, h_step = p0.result()
-    if world == 1 or W["scaling"] == "weak":
-        assert r_step == rows_expect, (r_step, rows_expect)
-    if world > 1 and W["scaling"] == "weak":   # rows of the whole batch, once, outside the timed region
+    if not collective:
+        assert r_step == rows_local, (r_step, rows_local)
+    if world > 1 and not collective:   # rows of the whole batch, once, outside the timed region
         rt = torch.tensor([r_step], dtype=torch.float64, device=dev)
         dist.all_reduce(rt, op=dist.ReduceOp.SUM)
         r_step = int(rt.item())
-
-    k5_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                 for _ in range(args.steps)]
+    k5_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     launches0 = fz.launch_count()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local_rank)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with sampler:
+    ctx = sampler if sampler is not None else _Null()
+    with ctx:
         e0.record(stream)
-        keep = []
-        for k in range(args.steps):
-            keep.append(step(k5_events[k]))
+        keep = [step(k5_ev[k]) for k in range(steps)]
         e1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = fz.launch_count() - launches0
-    ms_total = e0.elapsed_time(e1)
-    k5_ms = sum(a.elapsed_time(b) for a, b in k5_events) / args.steps
-    tt = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    ms = e0.elapsed_time(e1)
+    k5_ms = sum(a.elapsed_time(b) for a, b in k5_ev) / steps
+    tt = torch.tensor([ms, k5_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    ms_total = float(tt.item())
-    # r_step: every rank's rows of the step (N > 1: the all-reduced shard accumulators, or the batch sum)
-    rows_per_step = float(r_step)
-    value = rows_per_step * args.steps / (ms_total / 1e3)
-    r_local = rows_expect
+    ms_max, k5_max = float(tt[0]), float(tt[1])
+    del keep
+    return {"value": float(r_step) * steps / (ms_max / 1e3), "ms_per_step": ms_max / steps, "rows_step": int(r_step),
+            "rows_local": int(rows_local), "hash_step": int(h_step), "k5_ms": k5_ms, "k5_ms_max_rank": k5_max,
+            "launches": launches, "plan": p0, "fill_mode": lay.info["fill_mode"]}
 
-    # roofline of the dominant kernel (K5): algorithmic bytes per launch / its event time
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    if mode == "materialize":
-        alg_bytes = r_local * len(g) * 4
-        peak = peaks.get("hbm_gbs")
-        roof = {"kernel": f"k5_walk<{len(g)},{t},materialize>", "bound": "hbm",
-                "achieved": alg_bytes / (k5_ms / 1e3) / 1e9, "peak": peak if peak else 6650.0,
-                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md)",
-                "unit": "GB/s", "algorithmic_bytes_per_launch": alg_bytes}
-        roof["frac"] = roof["achieved"] / roof["peak"]
-    else:
-        # COUNT: one card lookup per leading prefix, 2 B each from the shared-memory copy
-        # of the card table; bound: the shared-memory crossbar, 128 B/clk/SM (B300_MICROARCH.md, LDS/STS)
-        # -> SMs x 128 / 2 lookups per clock at the max SM clock
-        U = leading_prefixes(g, n, len(g) - t)
-        # N > 1: the COUNT shards are cost-balanced, not unit-balanced; U / N is their mean
-        units = U // W["nshards"]
-        props = torch.cuda.get_device_properties(dev)
-        clk = sampler.summary().get("sm_max_mhz") or 1965
-        peak = props.multi_processor_count * 128 / 2 * clk * 1e6
-        roof = {"kernel": f"k5_walk<{len(g)},{t},count>", "bound": "alu", "achieved": units / (k5_ms / 1e3),
-                "unit": "card lookups/s (leading prefixes)", "peak": peak,
-                "peak_source": "derived: SMs x 128 B/clk shared-memory crossbar / 2 B per u16 card x max SM clock",
-                "algorithmic_units_per_launch": units, "frac": units / (k5_ms / 1e3) / peak}
-        if W["nshards"] > 1:
-            roof["units_note"] = "mean units per shard (cost-balanced COUNT cut)"
-    roof["traffic"] = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "k5_traffic.json")))
-        key = f"{W['name']}"
-        if key in prof:
-            roof["traffic"] = prof[key]["dram_bytes_per_launch"]
-    except Exception:
-        pass
-    roof["k5_ms"] = k5_ms
 
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def _leg_line(W, r, props, clk, world):
+    d = {"workload": f"{W['name']}: Z({W['n']}; {','.join(map(str, W['gens']))}) {W['mode']}, t={W['t']}",
+         "value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"], "rows": r["rows_step"],
+         "scaling": W["scaling"], "shards": W["nshards"]}
+    d["roofline"] = roofline(W, r["plan"], r["k5_ms"], r["rows_local"], clk, props, world)
+    return d
+
+
+def run_native(args, rank, world, local_rank, backend):
+    import torch
+
+    dev = torch.device("cuda", local_rank)
+    props = torch.cuda.get_device_properties(dev)
+    head_name = args.config or ("C2" if world == 1 else "C4")
+    W = workload(head_name, rank, world)
+    sampler = ClockSampler(local_rank)
+    r = measure(W, args.steps, args.warmup, rank, world, dev, sampler)
+    clocks = sampler.summary()
     res = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
         "scaling": W["scaling"], "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (fixed generator tuples; no datasets)",
-        "config": {"workload": f"{W['name']}: Z(n; {','.join(map(str, g))}) {mode}, memo t={t}, top=n+1",
-                   "n": n, "gens": list(g), "t": t, "mode": mode, "rows_per_rank_step": r_local,
-                   "fill_mode": lay.info["fill_mode"],
-                   "l2": ("each step writes its 1.6 GB output (> 126 MB L2), flushing L2 between steps"
-                          if mode == "materialize" else "count mode: tables L2-resident by design"),
-                   "parallelism": f"{'batch' if W['scaling'] == 'weak' else 'shard'}{world}"},
-        "gpu_launches": launches,
-        "roofline": roof,
-        "clocks": sampler.summary(),
+        "config": {"workload": f"{W['name']}: Z(n; {','.join(map(str, W['gens']))}) {W['mode']}, memo t={W['t']}, "
+                               f"top=n+1" + (f", cut into {world} shards (one problem)" if W["nshards"] > 1 else ""),
+                   "n": W["n"], "gens": list(W["gens"]), "t": W["t"], "mode": W["mode"],
+                   "rows_per_step": r["rows_step"], "rows_this_rank": r["rows_local"], "fill_mode": r["fill_mode"],
+                   "l2": ("each step writes its output (1.6 GB at N = 1, > 126 MB L2), flushing L2 between steps"
+                          if W["mode"] == "materialize" else
+                          "count mode: the card image is staged in shared memory each launch; tables L2-resident "
+                          "by design (no output)"),
+                   "parallelism": f"{'shard' if W['scaling'] == 'strong' and world > 1 else 'batch'}{world}"},
+        "gpu_launches": r["launches"],
+        "roofline": roofline(W, r["plan"], r["k5_ms"], r["rows_local"], clocks.get("sm_max_mhz"), props, world),
+        "clocks": clocks,
     }
     if world > 1:
-        res["config"]["collective"] = ("NCCL all_reduce(SUM) of the {rows, hash} shard accumulators each step"
-                                       if W["scaling"] == "strong" else
+        res["config"]["backend"] = backend
+        res["config"]["collective"] = ("all_reduce(SUM) of the 16-byte {rows, hash} shard accumulators each step "
+                                       f"over {backend}" if W["scaling"] == "strong" else
                                        "none in the data path (independent elements per rank)")
-    return res, (g, n, t, mode)
+    return res, W, r
 
 
-def count_mode_extra(local_rank):
-    """Count mode (the metric's second half) on this GPU: C2's element and C4 (t=3), whole step
-    (count tables + plan + the COUNT walk over every leading prefix), CUDA-event timed."""
+def native_legs(args, rank, world, local_rank, head):
+    """The other workloads on the same ranks (each timed like the headline): at N = 1 count C2 / C4 and hash
+    C3; at N > 1 C2 materialize row-sharded (strong) and the C2 batch (weak), plus C4 if not the headline."""
     import torch
 
-    from fzinputs import C2, C4
-    from paper_2407_20474_b200 import fz
-
-    res = {}
-    for name, g, n, t, steps in (("C2", C2.gens, C2.n, C2.t, 50), ("C4", C4.gens, C4.n, C4.t, 5)):
-        lay = fz.Layout(g, t, n + 1, entries=False)
-        ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device="cuda")
-        pws = torch.empty(256, dtype=torch.uint8, device="cuda")
-
-        def step():
-            m = fz.Memo(layout=lay, workspace=ws)
-            p = fz.Plan(m, n, "count", workspace=pws)
-            p.launch()
-            return m, p
-        for _ in range(3):
-            step()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        keep = [step() for _ in range(steps)]
-        e1.record()
-        torch.cuda.synchronize()
-        rows, _ = keep[-1][1].result()
-        ms = e0.elapsed_time(e1) / steps
-        res[name] = {"value": rows / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "rows": rows, "t": t,
-                     "workload": f"Z({n}; {','.join(map(str, g))}) count, t={t}"}
-    return res
+    dev = torch.device("cuda", local_rank)
+    props = torch.cuda.get_device_properties(dev)
+    legs = {}
+    if world == 1:
+        names = ["C4", "C2count"] if head != "C4" else ["C2"]
+    else:
+        names = [x for x in ("C2", "C2batch", "C4") if x != head]
+    for name in names:
+        if name == "C2count":
+            W = workload("C2", rank, world)
+            W = dict(W, name="C2count", mode="count")
+        else:
+            W = workload(name, rank, world)
+        steps = 20 if W["mode"] == "count" and W["name"].startswith("C4") else 50
+        r = measure(W, steps, 3, rank, world, dev)
+        legs[W["name"]] = _leg_line(W, r, props, None, world)
+    if world == 1 and not args.no_hash:
+        legs["C3hash"] = hash_leg(dev, props)
+    return legs
 
 
-def hash_mode_extra(local_rank):
-    """Hash mode on BASELINE.json configs[2] (C3: Z(17350; 23,29,31,37,41,43), 1.0e10 rows, t = 3 — the
-    fastest memo dimension): whole step (memo build + plan + the HASH walk), CUDA-event timed; the
-    (count, H) pair is compared with the known answer in tests/golden/hash_kats.csv."""
-    import torch
-
+def hash_leg(dev, props):
+    """Hash mode on BASELINE.json configs[2] (C3: Z(17350; 23,29,31,37,41,43), 1.0e10 rows, t = 3): whole
+    step (memo build + plan + the HASH walk), CUDA-event timed; (count, H) compared with the known answer in
+    tests/golden/hash_kats.csv."""
     from fzinputs import C3_GENS, C3_N
-    from paper_2407_20474_b200 import fz
 
-    g, n, t, steps = C3_GENS, C3_N, 3, 3
+    W = dict(name="C3hash", gens=C3_GENS, n=C3_N, t=3, mode="hash", shard=0, nshards=1, scaling="weak")
     kat = None
     for line in open(os.path.join(ROOT, "tests", "golden", "hash_kats.csv")):
         f = line.strip().split(",")
-        if len(f) >= 4 and f[0] == ";".join(map(str, g)) and f[1] == str(n):
+        if len(f) >= 4 and f[0] == ";".join(map(str, C3_GENS)) and f[1] == str(C3_N):
             kat = (int(f[2]), int(f[3], 16))
-    lay = fz.Layout(g, t, n + 1, entries=True)
-    ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device="cuda")
-    pws = None
-
-    def step():
-        nonlocal pws
-        m = fz.Memo(layout=lay, workspace=ws)
-        if pws is None:
-            pws = torch.empty(fz.plan_workspace_bytes(m), dtype=torch.uint8, device="cuda")
-        p = fz.Plan(m, n, "hash", workspace=pws)
-        p.launch()
-        return m, p
-    step()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    keep = [step() for _ in range(steps)]
-    e1.record()
-    torch.cuda.synchronize()
-    rows, h = keep[-1][1].result()
-    ms = e0.elapsed_time(e1) / steps
-    return {"C3": {"value": rows / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "rows": rows, "t": t,
-                   "hash": f"{h:#018x}", "kat_match": kat == (rows, h),
-                   "workload": f"Z({n}; {','.join(map(str, g))}) hash, t={t}"}}
+    r = measure(W, 3, 3, 0, 1, dev)
+    d = _leg_line(W, r, props, None, 1)
+    d["hash"] = f"{r['hash_step']:#018x}"
+    d["kat_match"] = kat == (r["rows_step"], r["hash_step"])
+    return d
 
 
-def run_e2e(args, spec, W, rank, world, local_rank):
+def run_e2e(args, W, rank, world, local_rank):
     """Same metric end to end through the public API from HOST buffers, on every rank; the timed region
     (barrier-bracketed, max over ranks) holds each step's H2D of the generator tuple and D2H of the result.
-    MATERIALIZE (weak, one element per rank): fz_run_host, rows streamed into pinned host memory.
-    COUNT (strong, one problem cut into shards): this rank's shard through Layout/Memo/Plan with the
-    NCCL all_reduce of {rows, hash}, then the 16-byte D2H read of the global result."""
+    MATERIALIZE: fz_run_host, rows streamed through the 64 MB device output ring into pinned host memory.
+    COUNT (one problem cut into shards): this rank's shard through Layout/Memo/Plan with the all_reduce
+    of {rows, hash}, then the 16-byte D2H read of the global result."""
     import torch
     import torch.distributed as dist
 
     from paper_2407_20474_b200 import fz
 
-    g, n, t, mode = spec
+    g, n, t, mode = W["gens"], W["n"], W["t"], W["mode"]
     d = len(g)
     dev = torch.device("cuda", local_rank)
     steps = max(1, min(args.steps, 3))
-    host = None
+    collective = world > 1 and W["scaling"] == "strong"
     if mode == "materialize":
-        ws = torch.empty(fz.run_workspace_bytes(g, t, n, mode), dtype=torch.uint8, device=dev)
-        lay = fz.Layout(g, t, n + 1, entries=True)
-        rows = fz.Plan(fz.Memo(layout=lay), n, mode).rows
+        # each rank streams its own element (the batch) or its shard's rows (row-sharded, via the same call on
+        # the whole element would repeat work): the e2e leg of materialize is the per-rank element
+        nn = n - rank if world > 1 else n
+        ws = torch.empty(fz.run_workspace_bytes(g, t, nn, mode), dtype=torch.uint8, device=dev)
+        lay = fz.Layout(g, t, nn + 1, entries=True)
+        rows = lay.shard_rows(nn, mode, 1)[1][0]
         host = torch.empty((rows, d), dtype=torch.int32).pin_memory()
 
         def one():
-            return fz.run_host(g, t, n, mode, host, workspace=ws)[0]
+            return fz.run_host(g, t, nn, mode, host, workspace=ws)[0]
     else:
         lay = fz.Layout(g, t, n + 1, entries=False)
         ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device=dev)
@@ -363,7 +415,7 @@ def run_e2e(args, spec, W, rank, world, local_rank):
                 pws = torch.empty(fz.plan_workspace_bytes(m), dtype=torch.uint8, device=dev)
             p = fz.Plan(m, n, mode, W["shard"], W["nshards"], workspace=pws)
             p.launch()
-            if world > 1:
+            if collective:
                 dist.all_reduce(p.result_tensor(), op=dist.ReduceOp.SUM)
             return p.result()[0]                            # D2H of {rows, hash}
     one()                                                   # warm-up
@@ -383,7 +435,7 @@ def run_e2e(args, spec, W, rank, world, local_rank):
         sm = el.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         el_s = float(mx[0])
-        tot = float(sm[1]) if W["scaling"] == "weak" else float(el[1])   # strong: all_reduced already
+        tot = float(el[1]) if collective else float(sm[1])   # strong: all_reduced already
     else:
         el_s = float(el[0])
     local_rows = int(el[1].item()) // steps
@@ -391,38 +443,26 @@ def run_e2e(args, spec, W, rank, world, local_rank):
             "d2h_bytes_per_step": (local_rows * d * 4 if mode == "materialize" else 0) + 16,
             "bytes_per": "rank and step",
             "steps": steps, "timing": "host wall clock around synchronised steps, max over ranks",
-            "api": ("fz_run_host (gens in host memory -> rows in pinned host memory), one element per rank"
-                    if mode == "materialize" else
+            "api": ("fz_run_host (gens in host memory -> rows streamed through the device output ring into pinned "
+                    "host memory), one element per rank" if mode == "materialize" else
                     "Layout/Memo/Plan (gens H2D each step) + all_reduce + fz_plan_result (16 B D2H)")}
 
 
-def leading_prefixes(g, n: int, L: int) -> int:
-    """Leading prefixes (a_1..a_L) with phi <= n = sum_{x<=n} |Z(x; g_1..g_L)| (coin-change counts;
-    measurement bookkeeping for the COUNT roofline, not part of the product path)."""
-    import numpy as np
-
-    c = np.zeros(n + 1, dtype=np.int64)
-    c[0] = 1
-    for gi in g[:L]:
-        for r in range(min(gi, n + 1)):
-            c[r::gi] = np.cumsum(c[r::gi])
-    return int(c.sum())
-
-
-def cpu_baseline(spec, budget_s: float = 12.0):
+def cpu_baseline(W, budget_s: float = 12.0):
     """The oracle as it stands (O1 nested loop + R17 hash, OpenMP over a_1) on this host's cores,
     on a bounded sample of the same workload: the a_1 range is cut into 64 contiguous chunks, visited
     from the fewest rows up (predicted by the oracle's GF counts) until the next chunk would overrun
     the budget at the rate measured so far (C2: the whole workload; C4: its high-a_1 chunks)."""
     from oracle import oracle as O
 
-    g, n, t, mode = spec
+    g, n = W["gens"], W["n"]
     C = O.C()
     threads = len(os.sched_getaffinity(0))
     top = n // g[0]
     nch = 64
     bounds = [(top + 1) * c // nch for c in range(nch + 1)]
     tail = C.gf_table(n, tuple(g[1:])) if len(g) > 1 else None      # |Z(x; g_2..g_d)|, x <= n
+
     def est(c):
         if tail is None:
             return 1
@@ -454,26 +494,42 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle on this host (rank 0 only), same config/metric/unit."""
     if rank != 0:
         return None
-    W = workload(args.config, 0, 1)
-    spec = (W["gens"], W["n"], W["t"], W["mode"])
+    n_gpus = max(world, args.gpus)
+    W = workload(args.config or ("C2" if n_gpus == 1 else "C4"), 0, 1)
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_baseline(spec, budget_s=per_step / 4)
+        cpu_baseline(W, budget_s=per_step / 4)
     vals, secs = [], 0.0
     last = None
     for _ in range(args.steps):
-        last = cpu_baseline(spec, budget_s=per_step)
+        last = cpu_baseline(W, budget_s=per_step)
         vals.append(last["value"])
         secs += last["seconds"]
     v = sorted(vals)[len(vals) // 2]
     last["value"] = v
-    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs * 1e3 / max(1, args.steps), "higher_is_better": True,
-            "scaling": W["scaling"], "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "scaling": "strong" if W["mode"] == "count" else "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
             "config": {"workload": f"{W['name']}: Z(n; {','.join(map(str, W['gens']))}) {W['mode']} (CPU oracle sample)",
-                       "n": W["n"], "gens": list(W["gens"]), "mode": W["mode"]},
+                       "n": W["n"], "gens": list(W["gens"]), "t": W["t"], "mode": W["mode"]},
             "cpu_baseline": last,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: run the N ranks under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -482,10 +538,12 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C2", "C4"])
+    ap.add_argument("--config", default=None, choices=["C2", "C2batch", "C4", "C4t2"],
+                    help="headline workload (default: C2 at N = 1, C4 at N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-count", action="store_true")
+    ap.add_argument("--no-count", action="store_true", help="skip the extra legs")
+    ap.add_argument("--no-hash", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = _env_int("WORLD_SIZE", 1)
@@ -497,29 +555,38 @@ def main():
         if res is not None:
             print(json.dumps(res), flush=True)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
 
     import torch
     import torch.distributed as dist
 
-    # one process per GPU; FZ_BENCH_BACKEND=gloo lets several ranks share one GPU (CI / single-GPU checks)
-    local_rank = local_rank % max(1, torch.cuda.device_count())
+    ngpu = max(1, torch.cuda.device_count())
+    backend = "none"
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # one process per GPU over NCCL; with fewer GPUs than ranks (or FZ_BENCH_BACKEND=gloo) the ranks
+        # share GPUs over gloo (NCCL refuses two ranks on one device) and the line says so
+        backend = os.environ.get("FZ_BENCH_BACKEND", "nccl" if ngpu >= world else "gloo")
+        local_rank = local_rank % ngpu
         torch.cuda.set_device(local_rank)
-        backend = os.environ.get("FZ_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            ver = ".".join(map(str, torch.cuda.nccl.version()))
+            backend = f"nccl {ver} ({world} ranks on {world} GPUs)"
         else:
-            dist.init_process_group(backend)
-    res, spec = run_native(args, rank, world, local_rank)
+            dist.init_process_group("gloo")
+            backend = f"gloo ({world} ranks sharing {ngpu} GPU{'s' if ngpu > 1 else ''})"
+        if rank == 0:
+            print(f"[bench] communicator: {backend}", file=sys.stderr, flush=True)
+    res, W, _ = run_native(args, rank, world, local_rank, backend)
     if not args.no_e2e:
-        res["e2e"] = run_e2e(args, spec, workload(args.config, rank, world), rank, world, local_rank)
+        res["e2e"] = run_e2e(args, W, rank, world, local_rank)
+    if not args.no_count:
+        res["legs"] = native_legs(args, rank, world, local_rank, W["name"])
     if rank == 0:
         if world == 1 and not args.no_cpu:
-            res["cpu_baseline"] = cpu_baseline(spec)
-        if world == 1 and args.config == "C2" and not args.no_count:
-            res["count_mode"] = count_mode_extra(local_rank)
-            res["hash_mode"] = hash_mode_extra(local_rank)
+            res["cpu_baseline"] = cpu_baseline(W)
         print(json.dumps(res), flush=True)
     if world > 1:
         dist.barrier()

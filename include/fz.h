@@ -27,7 +27,9 @@
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *     stream).  Calls that return host scalars synchronise that stream; all
  *     others are asynchronous on it.
- *   - Coordinates are uint32; n, phi, counts, offsets and hashes are uint64.
+ *   - Coordinates are uint32; n, phi, counts, offsets and hashes are uint64.  Limits the kernels
+ *     enforce (FZ_ERANGE beyond them): top <= 2^28 (so n < 2^28), memo blocks < 2^26 rows, COUNT
+ *     tail blocks < 2^32 rows, every count < 2^64 (reading R15).
  */
 #ifndef FZ_H
 #define FZ_H
@@ -43,7 +45,8 @@ extern "C" {
 typedef enum {
     FZ_OK = 0,
     FZ_EINVAL = 1,  /* contract violation: d, t, gens, n >= top, null or misaligned pointer */
-    FZ_ERANGE = 2,  /* n >= 2^32, a count >= 2^64, or a memo block >= 2^32 rows */
+    FZ_ERANGE = 2,  /* top > 2^28 (n < 2^28), a count >= 2^64, a memo block >= 2^26 rows, or (COUNT)
+                       a tail block >= 2^32 rows */
     FZ_ECAP = 3,    /* memo bytes exceed the memory cap (default 8e9 B; fz_set_memo_cap) */
     FZ_ENOSPC = 4,  /* caller workspace or output buffer too small */
     FZ_ECUDA = 5    /* CUDA runtime error (message in fz_last_error) */
@@ -85,7 +88,7 @@ typedef struct {
  * (Alg 2/3's product F[m] for every m < top),
  * in which Z(n) is the block Memo[n].
  * Errors: FZ_EINVAL (d, t, gens, top = 0), FZ_ERANGE (a table entry >= 2^64,
- * top > 2^32), FZ_ECAP (memo rows * t * 4 B above the cap). */
+ * top > 2^28, a memo block >= 2^26 rows), FZ_ECAP (memo rows * t * 4 B above the cap). */
 fz_status fz_memo_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t top, int with_entries,
                                   uint64_t *bytes);
 
@@ -191,6 +194,16 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
                          uint64_t plan_bytes, void *stream, fz_plan **out);
 void fz_plan_free(fz_plan *p);
 
+/* Which K5 kernel an enumeration of this plan runs (diagnostics, roofline bookkeeping):
+ *   FZ_WALK_ROWS         k5_walk over memo blocks (MATERIALIZE / HASH, full memo)
+ *   FZ_WALK_DEEP         k5_deep (partial memo, n >= memo_top)
+ *   FZ_WALK_TABLE        k5_table (t = d: Z(n) is the block Memo[n])
+ *   FZ_WALK_COUNT_PAIRS  k5_pairs (COUNT, L >= 3: staged card image, pairs of innermost runs per lane)
+ *   FZ_WALK_COUNT_RUNS   k5_walk COUNT (L <= 2, or a card table that cannot be staged)
+ * card_bytes: bytes per card lookup of the COUNT walk (1 = u8 image, 2 = u16 image, 4 = u32 table; 0 otherwise). */
+enum { FZ_WALK_ROWS = 0, FZ_WALK_DEEP = 1, FZ_WALK_TABLE = 2, FZ_WALK_COUNT_PAIRS = 3, FZ_WALK_COUNT_RUNS = 4 };
+fz_status fz_plan_walk(const fz_plan *p, int *kind, int *card_bytes);
+
 /* This plan's shard as computed on the device: first global row, row count,
  * number of slices (synchronises `stream`). */
 fz_status fz_plan_shard(const fz_plan *p, void *stream, uint64_t *row_begin, uint64_t *rows, uint64_t *nslices);
@@ -227,15 +240,26 @@ fz_status fz_enumerate(const fz_memo *m, uint64_t n, fz_mode mode, int shard, in
                        uint64_t *rows_out, uint64_t *hash_out);
 
 /* ------------------------------------------------------- end to end -- */
-/* Whole path from HOST buffers (Alg 5 as one call):
- * copy gens in, build the memo (top = n + 1, full memo), plan, enumerate,
- * and for MATERIALIZE stream the rows back into the HOST buffer h_out
- * (u32[rows * d]; pinned memory recommended) in chunks that overlap the
- * device-to-host copies with the enumeration (Buffer ->
- * host).  d_ws must hold fz_run_workspace_bytes.  When the full memo would exceed the memo cap the
- * memo is partial (memo_top = FZ_MEMO_TOP_AUTO) instead of FZ_ECAP.
- * Synchronises `stream`. */
-fz_status fz_run_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, uint64_t *bytes);
+/* Whole path from HOST buffers (Alg 5 as one call): build the memo (top = n + 1, full
+ * memo; partial, memo_top = FZ_MEMO_TOP_AUTO, when the full one exceeds the memo cap),
+ * plan, enumerate, and for MATERIALIZE stream the rows into the HOST buffer h_out (u32[rows * d]; pinned
+ * memory recommended) through a bounded DEVICE OUTPUT RING (PAPER.md:267, 281-285:
+ * Outputs -> Buffer -> copyDeviceBufferToHostAndClear, flushed whenever a buffer is full): the output is
+ * cut into chunks of at most one ring slot (the K4 shard cut with one shard per chunk); each chunk is
+ * enumerated into its slot and copied to the host on a copy stream while later chunks are enumerated,
+ * and a slot is reused once its copy has drained (CUDA events).  Output larger than the GPU's memory
+ * streams through any ring size.
+ *
+ * d_ws (256-B aligned, caller-owned) is laid out as [memo | 4 plan headers + accumulator | output ring]:
+ * everything beyond the memo and the headers is the ring, split into 4 slots.
+ * fz_run_workspace_bytes returns the memo + headers + `ring_bytes` of ring (0 = default: what the output
+ * needs, at most 64 MB; COUNT/HASH need no ring); the result does not grow with |Z(n)| beyond that.
+ * The copy stream and ring events are created once per thread and device and reused; so is the host
+ * layout of the last (gens, t, n, mode) of the thread.  Synchronises `stream`.
+ * Errors: FZ_EINVAL (mode, gens, d, misaligned workspace), FZ_ENOSPC (workspace below memo + headers,
+ * no room for one row per slot, h_out smaller than |Z(n)|), and the errors of the steps. */
+fz_status fz_run_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, uint64_t ring_bytes,
+                                 uint64_t *bytes);
 fz_status fz_run_host(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, void *d_ws, uint64_t ws_bytes,
                       uint32_t *h_out, uint64_t h_out_capacity_rows, void *stream, uint64_t *rows_out,
                       uint64_t *hash_out);

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -27,8 +29,8 @@ namespace {
 
 thread_local std::string g_err;
 thread_local uint64_t g_launches = 0;
-uint64_t g_memo_cap = 8000000000ull;
-int g_fill_override = 0;               // 0 = automatic fill-mode choice
+std::atomic<uint64_t> g_memo_cap{8000000000ull};   // SPEC.md:237 (process-wide setting, read at layout creation)
+std::atomic<int> g_fill_override{0};               // 0 = automatic fill-mode choice (process-wide, ditto)
 bool g_fuse_memo = true;               // fill mode 5 inside K1's cooperative launch (FZ_FUSE_MEMO=0 to split)
 
 fz_status fail(fz_status st, const char *fmt, ...)
@@ -80,14 +82,26 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
+// SM count of the current device (cached per device id; 148 when no device is visible, e.g. host-only
+// shard queries on a machine without a GPU)
 int device_sms()
 {
-    static thread_local int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) {
+        cudaGetLastError();
+        return 148;
     }
+    if (dev < 64) {
+        const int c = cache[dev].load(std::memory_order_relaxed);
+        if (c > 0) return c;
+    }
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+        cudaGetLastError();
+        sms = 148;
+    }
+    if (dev < 64) cache[dev].store(sms, std::memory_order_relaxed);
     return sms;
 }
 
@@ -135,7 +149,7 @@ fz_status host_tables(const uint32_t *g, int d, int L, uint64_t top, HostTables 
 }
 
 struct Layout {
-    uint64_t S, W, cardT, off, offT, chunk, links, rows, counter, list, total;
+    uint64_t S, W, C, cardT, off, offT, chunk, links, rows, counter, list, total;
 };
 
 struct Sizing {
@@ -155,9 +169,13 @@ struct Sizing {
     uint8_t lg_a[FZ_MAX_D] = {0}, lg_b[FZ_MAX_D] = {0};   // fill mode 5: log2 lanes per x, per level and pass
     uint64_t smem_bytes = 0;    // fill mode 1: dynamic shared memory
     int fill_mode = 0;
+    uint64_t beta = 32;         // COUNT pair walk: cost of a run beyond its lookups (C tables)
+    uint64_t gamma = 0;         // COUNT pair walk: cost of an outer prefix beyond its runs (C tables)
     Layout lay{};
 };
 
+constexpr uint64_t kCountRunCost = 32;     // COUNT pair-walk cost model (card lookups): per innermost run
+constexpr uint64_t kCountOuterCost = 0;    // ... and per outer prefix
 constexpr uint64_t kSmemMax = 220 * 1024;   // dynamic shared memory budget of the ring fill
 constexpr int kMaxGrid = 1024;              // chunk scratch entries of the K1 grid
 
@@ -181,12 +199,20 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
     z.t = t;
     z.L = d - t;
     z.top = top;
+    {   // cost model of the COUNT pair-walk cut (in card lookups): FZ_COUNT_RUN_COST per innermost run,
+        // FZ_COUNT_OUTER_COST per outer prefix, beyond the lookups
+        const char *e = getenv("FZ_COUNT_RUN_COST");
+        z.beta = (e && *e) ? (uint64_t)strtoull(e, nullptr, 10) : kCountRunCost;
+        const char *e2 = getenv("FZ_COUNT_OUTER_COST");
+        z.gamma = (e2 && *e2) ? (uint64_t)strtoull(e2, nullptr, 10) : kCountOuterCost;
+    }
     const int L = z.L;
     const uint64_t *card = H.S.data() + (size_t)L * top;
+    const uint64_t g_cap = g_memo_cap.load();   // one snapshot of the process-wide cap per layout
     if (!with_entries || t == 0 || memo_top == FZ_MEMO_TOP_FULL) {
         memo_top = top;
     } else if (memo_top == FZ_MEMO_TOP_AUTO) {   // partial memo: longest prefix of x whose rows fit the cap
-        const uint64_t cap_rows = g_memo_cap / (4ull * t);
+        const uint64_t cap_rows = g_cap / (4ull * t);
         uint64_t e = 0, x = 0;
         while (x < top && e + card[x] <= cap_rows) e += card[x++];
         if (x == 0) return fail(FZ_ECAP, "even Memo[0] exceeds the memo cap");
@@ -224,9 +250,9 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
     z.window = win;
     uint64_t rows_bytes = 0;
     if (with_entries && t > 0) {
-        if (entries > (g_memo_cap / (4ull * t)))
+        if (entries > (g_cap / (4ull * t)))
             return fail(FZ_ECAP, "memo of %llu rows x %d coords exceeds the cap of %llu bytes",
-                        (unsigned long long)entries, t, (unsigned long long)g_memo_cap);
+                        (unsigned long long)entries, t, (unsigned long long)g_cap);
         rows_bytes = entries * 4ull * t;
         // fill mode 1 (k3_fill_ring): ring over the rows of [x0 - max(hmax, 2b), x0 + b) for every batch
         // (look-back window + the batch whose bulk store may still be reading), links in chunks of chb batches
@@ -320,6 +346,7 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
     uint64_t p = 256;                                   // header
     l.S = p;       p = align_up(p + 8ull * (d + 1) * top, 256);
     l.W = p;       p = align_up(p + 8ull * (L + 1) * top, 256);
+    l.C = p;       if (L >= 3) p = align_up(p + 8ull * (L - 2) * top, 256);   // COUNT cost tables C_0..C_{L-3}
     l.off = p;     p = align_up(p + 8ull * (top + 1), 256);
     l.cardT = p;   p = align_up(p + 4ull * (top + m), 256);
     l.offT = p;    p = align_up(p + 8ull * (top + m), 256);
@@ -349,11 +376,22 @@ struct fz_memo {
     const fz_layout *lay;
     fz_layout *owned;      // layout created by fz_memo_build (freed with the memo)
     char *ws;
-    uint64_t *S, *W, *off, *offT, *chunk;
+    uint64_t *S, *W, *C, *off, *offT, *chunk;
     uint32_t *cardT, *rows;
     void *links;
     unsigned int *counter;
 };
+
+namespace {
+// COUNT pair walk (k5_pairs, L >= 3): geometry of the staged card image, or on = false when the walk
+// cannot stage it (cards too large, image above the shared-memory budget) or FZ_COUNT_SMEM=0.
+struct PairPlan {
+    bool on = false, u8 = false;
+    fzk::PairGeo pg{};
+    uint32_t f0n = 0;
+    size_t smem = 0;
+};
+}  // namespace
 
 struct fz_plan {
     const fz_memo *m;
@@ -361,6 +399,7 @@ struct fz_plan {
     fz_mode mode;
     int shard, nshards;
     char *d_plan;
+    PairPlan pp;
 };
 
 // ------------------------------------------------------------ launch helpers
@@ -406,6 +445,111 @@ fzk::ProgGens make_prog(const uint32_t *g, int d)
     P.me = magic(P.e);
     P.mh1 = magic(P.h1);
     return P;
+}
+
+
+constexpr uint64_t kPairSmemMax = 220 * 1024;   // dynamic shared memory of one k5_pairs CTA (one per SM)
+
+PairPlan pair_plan(const fz_layout *lay, uint64_t n)
+{
+    PairPlan P;
+    const Sizing &z = lay->z;
+    const int L = z.L;
+    if (L < 3) return P;
+    const char *env = getenv("FZ_COUNT_SMEM");
+    if (env && env[0] == '0') return P;
+    const uint64_t cmax = z.card_max_all;
+    const uint32_t m = lay->g[L - 1], g2 = lay->g[L - 2];
+    if (m >= 65536) return P;
+    // packed accumulators: a byte (u8) / half (u16) takes 4 cards of the two masked last vectors
+    const bool u8 = cmax <= 63;
+    if (!u8 && cmax > 16383) return P;
+    const uint64_t q = n / m + 1;                    // longest column prefix of a run
+    if (2 * q * cmax >= (1ull << 32)) return P;      // per-pair u32 sum
+    const uint64_t VE = u8 ? 16 : 8, eb = u8 ? 1 : 2;
+    // > q entries per column (a run's pointer never leaves its column: k5_pairs' merged loop), rounded to
+    // whole vectors, an odd number of them (the 16-B vectors of 8 consecutive columns: 8 bank groups)
+    uint64_t R16 = (q + 1 + VE - 1) / VE * VE;
+    if ((R16 / VE) % 2 == 0) R16 += VE;
+    const uint32_t dlt = g2 % m;
+    uint32_t e = m, y = dlt;                         // e = gcd(Delta, m) (gcd(0, m) = m)
+    while (y) {
+        const uint32_t r = e % y;
+        e = y;
+        y = r;
+    }
+    const uint32_t mp = m / e;
+    const uint64_t f0 = n / lay->g[0] + 1;
+    const uint32_t f0n = (f0 <= 4096) ? (uint32_t)f0 : 0u;
+    const uint64_t f0b = (uint64_t)(f0n + 1) / 2 * 16;
+    auto bytes = [&](uint64_t dd) { return f0b + (uint64_t)e * (mp + dd) * R16 * eb; };
+    uint32_t dup = 31;
+    if (bytes(31) > kPairSmemMax) dup = 0;
+    if (bytes(dup) > kPairSmemMax) return P;
+    // inverse of Delta / e modulo m' (extended Euclid; 0 when m' = 1)
+    uint32_t inv = 0;
+    if (mp > 1) {
+        int64_t r0 = mp, r1 = (dlt / e) % mp, s0 = 0, s1 = 1;
+        while (r1) {
+            const int64_t qq = r0 / r1, r2 = r0 - qq * r1, s2 = s0 - qq * s1;
+            r0 = r1;
+            r1 = r2;
+            s0 = s1;
+            s1 = s2;
+        }
+        inv = (uint32_t)(((s0 % (int64_t)mp) + mp) % mp);
+    }
+    fzk::PairGeo &g = P.pg;
+    g.m = m;
+    g.dlt = dlt;
+    g.e = e;
+    g.mp = mp;
+    g.dup = dup;
+    g.inv = inv;
+    g.R16 = (uint32_t)R16;
+    g.ncolv = e * (mp + dup);
+    // flush period (iterations of 4 cards per packed lane: a Y and an X word pair)
+    g.F = cmax == 0 ? (1u << 30) : (uint32_t)((u8 ? 255ull : 65535ull) / (4 * cmax));
+    auto m32 = [](uint64_t v) -> uint32_t { return v == 1 ? 0xffffffffu : (uint32_t)((1ull << 32) / v); };
+    g.Mm = m32(m);
+    g.Mg2 = m32(g2);
+    g.Me = m32(e);
+    g.Mmp = m32(mp);
+    for (int j = 0; j < FZ_MAX_D; ++j) g.Mg[j] = m32(j < z.d ? lay->g[j] : 1);
+    // the common outer step R += g3 (k5_pairs advance): g3 = Q3 g2 + S3; column steps mod m for the two
+    // outcomes of rmin + S3 >= g2, and their orbit-position steps when e = 1
+    const uint32_t g3 = lay->g[L - 3];
+    g.Q3 = g3 / g2;
+    g.S3 = g3 % g2;
+    g.cs1 = g.S3 % m;
+    g.cs2 = (uint32_t)(((uint64_t)g.S3 % m + m - g2 % m) % m);
+    g.is1 = e == 1 ? (uint32_t)((uint64_t)g.cs1 * inv % m) : 0;
+    g.is2 = e == 1 ? (uint32_t)((uint64_t)g.cs2 * inv % m) : 0;
+    P.on = true;
+    P.u8 = u8;
+    P.f0n = f0n;
+    P.smem = (size_t)bytes(dup);
+    return P;
+}
+
+// host copy of the device cost tables C_0..C_{L-3} (same integer arithmetic as K1)
+std::vector<uint64_t> host_cost_tables(const fz_layout *lay)
+{
+    const int L = lay->z.L;
+    const uint64_t top = lay->z.top, beta = lay->z.beta, gamma = lay->z.gamma;
+    std::vector<uint64_t> C((size_t)(L - 2) * top, 0);
+    const uint64_t *W2 = lay->H.W.data() + (size_t)(L - 2) * top;
+    const uint64_t g2 = lay->g[L - 2];
+    for (int jc = L - 3; jc >= 0; --jc) {
+        const uint64_t gj = lay->g[jc];
+        uint64_t *Cj = C.data() + (size_t)jc * top;
+        const uint64_t *Cn = (jc + 1 <= L - 3) ? C.data() + (size_t)(jc + 1) * top : nullptr;
+        for (uint64_t x = 0; x < top; ++x) {
+            const uint64_t src = Cn ? Cn[x] : W2[x] + beta * (x / g2 + 1) + gamma;
+            Cj[x] = src + (x >= gj ? Cj[x - gj] : 0);
+        }
+    }
+    return C;
 }
 
 constexpr uint64_t kPlanHeader = 256;
@@ -542,20 +686,16 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     // level-0 unrank column in shared memory when it is short (<= 4096 entries, 32 KB)
     const uint64_t f0 = a.n / a.G.g[0] + 1;
     const uint32_t f0n = (f0 <= 4096) ? (uint32_t)f0 : 0u;
-    // COUNT: the residue-major card table as u16 in shared memory when its values and size allow
-    // FZ_COUNT_SMEM=0 never stages the table, =2 stages it whatever the walk size (tests)
+    // COUNT with L = 2: the residue-major card table as u16 in shared memory (x <= n, R16 entries per
+    // column: a multiple of 8 with R16 / 8 odd, so the 16-B vector loads of 8 lanes in different columns hit
+    // distinct banks) when its values and size allow and the walk has enough prefixes per CTA to repay
+    // the staging.  FZ_COUNT_SMEM=0 never stages the table, =2 stages it whatever the walk size (tests).
     const char *c16e = getenv("FZ_COUNT_SMEM");
     const bool c16_env = !(c16e && c16e[0] == '0'), c16_force = c16e && c16e[0] == '2';
-    // (x <= n, residue-major with R16 entries per column: a multiple of 8 with R16 / 8 odd, so the
-    // 16-B vector loads of 8 lanes in different columns hit distinct banks), when the walk has enough
-    // prefixes per CTA to repay the staging
-    // u8 entries (16 per vector, R16 / 16 odd) when every card < 256 and the outer-prefix walk runs (L >= 3)
-    const bool u8 = MODE == FZ_COUNT && D - T >= 3 && a.card_max < 256;
-    const uint64_t per_vec = u8 ? 16 : 8;
-    uint64_t R16 = (a.n / a.wt.m + 1 + per_vec - 1) / per_vec * per_vec;
-    if ((R16 / per_vec) % 2 == 0) R16 += per_vec;
-    const uint64_t cbytes = R16 * a.wt.m * (u8 ? 1 : 2);
-    const uint32_t c16R = (MODE == FZ_COUNT && D - T >= 2 && c16_env && a.card_max < 65536 &&
+    uint64_t R16 = (a.n / a.wt.m + 1 + 7) / 8 * 8;
+    if ((R16 / 8) % 2 == 0) R16 += 8;
+    const uint64_t cbytes = R16 * a.wt.m * 2;
+    const uint32_t c16R = (MODE == FZ_COUNT && D - T == 2 && c16_env && a.card_max < 65536 &&
                            a.card_max * (a.n / a.wt.m + 1) < (1ull << 32) &&   // per-lane u32 run sums
                            cbytes + f0n * 8 + 8 <= kCountSmemMax &&
                            (c16_force || a.prefixes >= (a.n + 1) * 64 * (uint64_t)device_sms()))
@@ -563,38 +703,49 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
                               : 0u;
     const size_t smem = (size_t)(f0n + 1) / 2 * 16 + (c16R ? cbytes : 0);
     // persistent grid: exactly the resident CTAs (the walk is a grid-stride loop over slices)
-    static thread_local size_t last_smem = ~(size_t)0;
-    static thread_local int per_sm = 0;
-    if (smem != last_smem) {
-        if (smem > 48 * 1024) {
-            FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-            if constexpr (MODE == FZ_COUNT && D - T >= 3)
-                FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        }
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::walk_threads<MODE>(),
-                                                          std::max<size_t>(smem, 4096 * 8)) != cudaSuccess ||
-            per_sm < 1)
-            per_sm = 1;
-        per_sm = std::min(per_sm, 8);
-        last_smem = smem;
-    }
-    auto go = [&](auto kern) {
-        return launch_pdl(kern, dim3((unsigned)(device_sms() * per_sm)), dim3(fzk::walk_threads<MODE>()), smem, s, a.G,
-                          (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top, a.wt, a.out, (uint64_t)a.cap,
-                          (uint64_t)a.row_base, f0n, c16R);
-    };
-    if constexpr (MODE == FZ_COUNT && D - T >= 3) {
-        if (u8 && c16R)
-            FZ_CUDA(go(fzk::k5_walk<D, T, MODE, true>));
-        else
-            FZ_CUDA(go(fzk::k5_walk<D, T, MODE, false>));
-    } else {
-        FZ_CUDA(go(fzk::k5_walk<D, T, MODE, false>));
-    }
+    int per_sm = 0;
+    // (static shared memory -- the MATERIALIZE word-stream staging -- plus this dynamic part may pass 48 KB)
+    FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::walk_threads<MODE>(),
+                                                      std::max<size_t>(smem, 4096 * 8)) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    per_sm = std::min(per_sm, 8);
+    FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE>, dim3((unsigned)(device_sms() * per_sm)),
+                       dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
+                       a.wt, a.out, (uint64_t)a.cap, (uint64_t)a.row_base, f0n, c16R));
     ++g_launches;
     return cuda_check("k5_walk");
+}
+
+// COUNT pair walk (L >= 3): one 1024-thread CTA per SM (the K4 guided slices assume exactly that grid)
+template <int D, int T = 0>
+fz_status launch_pairs_d(int t, const PairPlan &pp, const WalkArgs &a, const uint64_t *C, const uint32_t *cardT,
+                         uint64_t Rcol, cudaStream_t s)
+{
+    if constexpr (T + 3 <= D) {
+        if (t != T) return launch_pairs_d<D, T + 1>(t, pp, a, C, cardT, Rcol, s);
+        auto kern = pp.u8 ? fzk::k5_pairs<D, T, true> : fzk::k5_pairs<D, T, false>;
+        FZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem));
+        FZ_CUDA(launch_pdl(kern, dim3((unsigned)device_sms()), dim3(fzk::kCountThreads), pp.smem, s, a.G,
+                           (uint64_t)a.n, a.hdr, C, (uint64_t)a.top, cardT, Rcol, pp.pg, pp.f0n));
+        ++g_launches;
+        return cuda_check("k5_pairs");
+    } else {
+        return fail(FZ_EINVAL, "pair walk: t=%d not instantiated for d=%d", t, D);
+    }
+}
+
+template <int D = 3>
+fz_status launch_pairs(int d, int t, const PairPlan &pp, const WalkArgs &a, const uint64_t *C, const uint32_t *cardT,
+                       uint64_t Rcol, cudaStream_t s)
+{
+    if constexpr (D <= FZ_MAX_D) {
+        if (d == D) return launch_pairs_d<D>(t, pp, a, C, cardT, Rcol, s);
+        return launch_pairs<D + 1>(d, t, pp, a, C, cardT, Rcol, s);
+    } else {
+        return fail(FZ_EINVAL, "d=%d not instantiated", d);
+    }
 }
 
 template <int D, int T = 0>
@@ -649,14 +800,10 @@ fz_status launch_deep_dt(int mode, const WalkArgs &a, const uint64_t *S, uint64_
                          cudaStream_t s)
 {
     auto kern = (mode == FZ_MATERIALIZE) ? fzk::k5_deep<D, T, FZ_MATERIALIZE> : fzk::k5_deep<D, T, FZ_HASH>;
-    static thread_local int per_sm[2] = {0, 0};
-    int &ps = per_sm[mode == FZ_MATERIALIZE ? 0 : 1];
-    if (!ps) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, fzk::kWalkThreads, 4096 * 8) != cudaSuccess ||
-            ps < 1)
-            ps = 2;
-        ps = std::min(ps, 8);
-    }
+    int ps = 0;   // resident CTAs per SM (queried per launch: no per-thread cache that could outlive a device switch)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, fzk::kWalkThreads, 4096 * 8) != cudaSuccess || ps < 1)
+        ps = 2;
+    ps = std::min(ps, 8);
     // closed form of the last two coordinates (PROG leaves): Z(x; g, h), g = g_{d-2}, h = g_{d-1}
     uint32_t gg[D];
     for (int j = 0; j < D; ++j) gg[j] = a.G.g[j];
@@ -694,11 +841,12 @@ fz_status launch_deep(int d, int t, int mode, const WalkArgs &a, const uint64_t 
 }
 
 // host-side rank / unrank over the layout's host tables (fz_shard_rows, fz_run_host)
-uint64_t host_row_rank(const fz_layout *lay, uint64_t n, const uint32_t *a)
+// global row of the first row of prefix a_1..a_levels: sum_j S_j[r_j - (a_j + 1) g_j]
+uint64_t host_row_rank(const fz_layout *lay, uint64_t n, const uint32_t *a, int levels)
 {
     const uint64_t top = lay->z.top;
     uint64_t r = n, R = 0;
-    for (int j = 0; j < lay->z.L; ++j) {
+    for (int j = 0; j < levels; ++j) {
         const uint64_t nxt = (uint64_t)(a[j] + 1ull) * lay->g[j];
         if (nxt <= r) R += lay->H.S[(size_t)j * top + (r - nxt)];
         r -= (uint64_t)a[j] * lay->g[j];
@@ -706,12 +854,14 @@ uint64_t host_row_rank(const fz_layout *lay, uint64_t n, const uint32_t *a)
     return R;
 }
 
-void host_unrank_prefix(const fz_layout *lay, uint64_t n, uint64_t R, uint32_t *a)
+// unrank R over `levels` levels of a unit table T (level j: T[j][r - a g_j] = units with a'_j >= a);
+// returns the rank left inside the prefix reached (same search as the device unrank)
+uint64_t host_unrank(const fz_layout *lay, const uint64_t *T, uint64_t n, int levels, uint64_t R, uint32_t *a)
 {
     const uint64_t top = lay->z.top;
     uint64_t r = n;
-    for (int j = 0; j < lay->z.L; ++j) {
-        const uint64_t *Tj = lay->H.W.data() + (size_t)j * top;
+    for (int j = 0; j < levels; ++j) {
+        const uint64_t *Tj = T + (size_t)j * top;
         const uint64_t gj = lay->g[j], amax = r / gj;
         uint64_t lo = 0, hi = amax;   // largest a with Tj[r - a gj] > R
         while (lo < hi) {
@@ -722,90 +872,78 @@ void host_unrank_prefix(const fz_layout *lay, uint64_t n, uint64_t R, uint32_t *
         R -= (lo + 1 <= amax) ? Tj[r - (lo + 1) * gj] : 0;
         r -= lo * gj;
     }
+    return R;
+}
+
+// nextCandidate over the first nl coordinates (host twin of fzk::prefix_next)
+bool host_prefix_next(const fz_layout *lay, uint32_t *a, int nl, uint64_t n)
+{
+    int i = -1;
+    for (int j = 0; j < nl; ++j)
+        if (a[j] > 0) i = j;
+    if (i < 0) return false;
+    uint64_t r = n;
+    for (int j = 0; j < nl; ++j) {
+        if (j == i) a[j] -= 1;
+        if (j > i) a[j] = (uint32_t)(r / lay->g[j]);
+        r -= (uint64_t)a[j] * lay->g[j];
+    }
+    return true;
 }
 
 uint64_t mul_div_h(uint64_t U, uint64_t a, uint64_t b) { return (U / b) * a + ((U % b) * a) / b; }
 
-// COUNT shard cut balanced by cost instead of leading prefixes: a prefix costs 1 (its card lookup) and each
-// innermost run (a_1..a_{L-1} fixed) costs beta more (its per-run bookkeeping in the walk), i.e. the table
-// C_j = W_j + beta V_j (V_j counts the runs; the same column-scan recurrence as W). Shard s starts at the
-// leading prefix holding cost rank C_0[n] s / k; its W-rank is the unit boundary K4 uses. Any boundary is
-// an exact cover, so the cut only moves work between shards. FZ_COUNT_RUN_COST sets beta (0: plain cut).
-uint64_t count_cut(const fz_layout *lay, uint64_t n, int nshards, int s)
-{
-    const uint64_t P = lay->H.W[n];
-    static const uint64_t beta = [] {
-        const char *e = getenv("FZ_COUNT_RUN_COST");
-        return (e && *e) ? (uint64_t)strtoull(e, nullptr, 10) : (uint64_t)32;
-    }();
-    const int L = lay->z.L;
-    if (s <= 0) return 0;
-    if (s >= nshards) return P;
-    if (beta == 0 || L < 2) return mul_div_h(P, (uint64_t)s, (uint64_t)nshards);
-    const uint64_t top = n + 1;
-    // C_{L}[x] = 1 (one lookup), C_{L-1}[x] = x / g_{L-1} + 1 + beta, C_j = column scan of C_{j+1} by g_j;
-    // cached per thread for the last (layout, n) (a plan per step must not rebuild it)
-    static thread_local uint32_t c_g[FZ_MAX_D];
-    static thread_local int c_L = -1, c_d = -1;
-    static thread_local uint64_t c_n = ~0ull;
-    static thread_local std::vector<uint64_t> C;
-    bool hit = c_L == L && c_d == lay->z.d && c_n == n;
-    for (int j = 0; hit && j < lay->z.d; ++j) hit = c_g[j] == lay->g[j];
-    if (!hit) {
-        C.assign((size_t)(L + 1) * top, 0);
-        for (uint64_t x = 0; x < top; ++x) {
-            C[(size_t)L * top + x] = 1;
-            C[(size_t)(L - 1) * top + x] = x / lay->g[L - 1] + 1 + beta;
-        }
-        for (int j = L - 2; j >= 0; --j) {
-            const uint64_t gj = lay->g[j];
-            uint64_t *Cj = C.data() + (size_t)j * top;
-            const uint64_t *Cn = Cj + top;
-            for (uint64_t x = 0; x < top; ++x) Cj[x] = Cn[x] + (x >= gj ? Cj[x - gj] : 0);
-        }
-        for (int j = 0; j < lay->z.d; ++j) c_g[j] = lay->g[j];
-        c_L = L;
-        c_d = lay->z.d;
-        c_n = n;
-    }
-    const uint64_t total = C[n];
-    uint64_t R = mul_div_h(total, (uint64_t)s, (uint64_t)nshards);
-    // unrank the cost rank R (descending lex, as host_unrank_prefix) and take that prefix's W-rank
-    uint64_t r = n, wrank = 0;
-    for (int j = 0; j < L; ++j) {
-        const uint64_t gj = lay->g[j], amax = r / gj;
-        // cumulative cost of the candidates a_j = amax .. a+1: sum_{a' > a} Tj[r - a' gj] = C_j[r - (a+1) gj]
-        const uint64_t *Cj = C.data() + (size_t)j * top;
-        uint64_t lo = 0, hi = amax;   // largest a with C_j[r - a gj] > R
-        while (lo < hi) {
-            const uint64_t mid = lo + (hi - lo + 1) / 2;
-            if (Cj[r - mid * gj] > R) lo = mid; else hi = mid - 1;
-        }
-        R -= (lo + 1 <= amax) ? Cj[r - (lo + 1) * gj] : 0;   // (at j = L-1, C carries the run's beta: last level)
-        if (lo + 1 <= amax) wrank += lay->H.W[(size_t)j * lay->z.top + (r - (lo + 1) * gj)];
-        r -= lo * gj;
-    }
-    return wrank < P ? wrank : P;
-}
-
-// same shard cut as k4_plan, on the host tables
-void host_shard(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, int s, uint64_t &rb, uint64_t &rl)
+// same shard cut as k4_plan, on the host tables.  C: host_cost_tables when the COUNT pair walk runs.
+void host_shard(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, int s, uint64_t &rb, uint64_t &rl,
+                const std::vector<uint64_t> *C)
 {
     const uint64_t rows_total = lay->H.S[n];
-    if (mode == FZ_COUNT && lay->z.L > 0) {
+    const int L = lay->z.L;
+    if (mode == FZ_COUNT && C) {   // pair walk: cost ranks, whole outer prefixes
+        const uint64_t U = (*C)[n];
+        auto rowat = [&](uint64_t u) -> uint64_t {
+            if (u >= U) return rows_total;
+            uint32_t a[FZ_MAX_D] = {0};
+            if (host_unrank(lay, C->data(), n, L - 2, u, a) != 0 && !host_prefix_next(lay, a, L - 2, n))
+                return rows_total;
+            return host_row_rank(lay, n, a, L - 2);
+        };
+        rb = rowat(mul_div_h(U, s, nshards));
+        rl = rowat(mul_div_h(U, s + 1, nshards)) - rb;
+    } else if (mode == FZ_COUNT && L > 0) {   // leading prefixes
         const uint64_t P = lay->H.W[n];
         auto rowat = [&](uint64_t pidx) -> uint64_t {
             if (pidx >= P) return rows_total;
             uint32_t a[FZ_MAX_D] = {0};
-            host_unrank_prefix(lay, n, pidx, a);
-            return host_row_rank(lay, n, a);
+            host_unrank(lay, lay->H.W.data(), n, L, pidx, a);
+            return host_row_rank(lay, n, a, L);
         };
-        rb = rowat(count_cut(lay, n, nshards, s));
-        rl = rowat(count_cut(lay, n, nshards, s + 1)) - rb;
+        rb = rowat(mul_div_h(P, s, nshards));
+        rl = rowat(mul_div_h(P, s + 1, nshards)) - rb;
     } else {
         rb = mul_div_h(rows_total, s, nshards);
         rl = mul_div_h(rows_total, s + 1, nshards) - rb;
     }
+}
+
+// host shard cut of every shard (fz_shard_rows, fz_layout_shard_rows)
+fz_status host_shards(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, uint64_t *row_begin,
+                      uint64_t *rows)
+{
+    try {
+        std::vector<uint64_t> C;
+        const bool pairs = mode == FZ_COUNT && pair_plan(lay, n).on;
+        if (pairs) C = host_cost_tables(lay);
+        for (int s = 0; s < nshards; ++s) {
+            uint64_t rb, rl;
+            host_shard(lay, n, mode, nshards, s, rb, rl, pairs ? &C : nullptr);
+            if (row_begin) row_begin[s] = rb;
+            if (rows) rows[s] = rl;
+        }
+    } catch (const std::bad_alloc &) {
+        return fail(FZ_ECAP, "host cost tables do not fit host memory");
+    }
+    return FZ_OK;
 }
 
 fz_status make_layout(const uint32_t *gens, int d, int t, uint64_t top, int with_entries, fz_layout **out,
@@ -910,6 +1048,7 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
     m->ws = w;
     m->S = (uint64_t *)(w + z.lay.S);
     m->W = (uint64_t *)(w + z.lay.W);
+    m->C = z.L >= 3 ? (uint64_t *)(w + z.lay.C) : nullptr;
     m->off = (uint64_t *)(w + z.lay.off);
     m->cardT = (uint32_t *)(w + z.lay.cardT);
     m->offT = (uint64_t *)(w + z.lay.offT);
@@ -922,6 +1061,9 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
     fzk::Tables tb;
     tb.S = m->S;
     tb.W = m->W;
+    tb.C = m->C;
+    tb.beta = z.beta;
+    tb.gamma = z.gamma;
     tb.off = m->off;
     tb.cardT = m->cardT;
     tb.offT = m->offT;
@@ -1023,13 +1165,8 @@ fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards,
 {
     if (!m || nshards < 1) return fail(FZ_EINVAL, "NULL memo or nshards < 1");
     if (n >= m->lay->z.top) return fail(FZ_EINVAL, "n >= top");
-    for (int s = 0; s < nshards; ++s) {
-        uint64_t rb, rl;
-        host_shard(m->lay, n, mode, nshards, s, rb, rl);
-        if (row_begin) row_begin[s] = rb;
-        if (rows) rows[s] = rl;
-    }
-    return FZ_OK;
+    if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode");
+    return host_shards(m->lay, n, mode, nshards, row_begin, rows);
 }
 
 // SURVEY §8(f) f4 (the best memo dimension depends on the instance).  Predicted
@@ -1091,13 +1228,7 @@ fz_status fz_layout_shard_rows(const fz_layout *lay, uint64_t n, fz_mode mode, i
     if (!lay || nshards < 1) return fail(FZ_EINVAL, "NULL layout or nshards < 1");
     if (n >= lay->z.top) return fail(FZ_EINVAL, "n >= top");
     if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode");
-    for (int s = 0; s < nshards; ++s) {
-        uint64_t rb, rl;
-        host_shard(lay, n, mode, nshards, s, rb, rl);
-        if (row_begin) row_begin[s] = rb;
-        if (rows) rows[s] = rl;
-    }
-    return FZ_OK;
+    return host_shards(lay, n, mode, nshards, row_begin, rows);
 }
 
 fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t *bytes)
@@ -1122,6 +1253,9 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
                     (unsigned long long)z.top);
     if (mode != FZ_COUNT && z.t > 0 && z.fill_mode == 0)
         return fail(FZ_EINVAL, "memo built without entries; only FZ_COUNT is possible");
+    if (mode == FZ_COUNT && z.card_max_all >= (1ull << 32))   // the walk reads the u32 card table (K2 cardT)
+        return fail(FZ_ERANGE, "a tail block has %llu >= 2^32 rows (COUNT walk reads u32 cards)",
+                    (unsigned long long)z.card_max_all);
     if (!d_plan || ((uintptr_t)d_plan & 255)) return fail(FZ_EINVAL, "plan workspace NULL or misaligned");
     if (plan_ws_bytes < plan_bytes())
         return fail(FZ_ENOSPC, "plan workspace %llu B < required %llu B", (unsigned long long)plan_ws_bytes,
@@ -1137,24 +1271,23 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
     PlanArgs A;
     A.n = n;
     A.top = z.top;
-    // COUNT shards of a 4-way or wider cut take half the slices (each shard re-pays the slice starts;
-    // measured: 8 shards 0.71 -> 0.74 of linear, one shard 1 % slower)
-    A.max_slices = max_slices(mode) / ((mode == FZ_COUNT && nshards >= 4) ? 2 : 1);
+    A.max_slices = max_slices(mode);
     A.floor_len = (mode == FZ_COUNT) ? 1024 : 32;
     A.mode = (int)mode;
     A.shard = shard;
     A.nshards = nshards;
     A.L = z.L;
-    A.cut_given = 0;
-    A.ub = A.ue = 0;
-    if (mode == FZ_COUNT && z.L > 0 && nshards > 1) {   // cost-balanced COUNT cut (host tables)
-        A.cut_given = 1;
-        A.ub = count_cut(m->lay, n, nshards, shard);
-        A.ue = count_cut(m->lay, n, nshards, shard + 1);
+    p->pp = (mode == FZ_COUNT) ? pair_plan(m->lay, n) : PairPlan{};
+    A.pairs = p->pp.on ? 1 : 0;
+    A.wg = (uint64_t)device_sms() * (fzk::kCountThreads / 32);   // k5_pairs: one 1024-thread CTA per SM
+    {
+        const char *e = getenv("FZ_GSS_TAIL");                    // last slices ~ 1/tail of a warp's share
+        A.gss_tail = (e && atoi(e) > 0) ? (uint64_t)atoi(e) : 128;
     }
     Gens G = make_gens(m->lay->g, z.d);
     const cudaError_t le = launch_pdl(fzk::k4_plan, dim3(1), dim3(32), 0, (cudaStream_t)stream, G, A,
-                                      (const uint64_t *)m->S, (const uint64_t *)m->W, (PlanHdr *)p->d_plan);
+                                      (const uint64_t *)m->S, (const uint64_t *)m->W, (const uint64_t *)m->C,
+                                      (PlanHdr *)p->d_plan);
     if (le != cudaSuccess) {
         delete p;
         return fail(FZ_ECUDA, "k4_plan launch: %s", cudaGetErrorString(le));
@@ -1170,6 +1303,29 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
 }
 
 void fz_plan_free(fz_plan *p) { delete p; }
+
+fz_status fz_plan_walk(const fz_plan *p, int *kind, int *card_bytes)
+{
+    if (!p) return fail(FZ_EINVAL, "NULL plan");
+    const Sizing &z = p->m->lay->z;
+    int k = FZ_WALK_ROWS, cb = 0;
+    if (p->mode == FZ_COUNT && z.L > 0) {
+        if (p->pp.on) {
+            k = FZ_WALK_COUNT_PAIRS;
+            cb = p->pp.u8 ? 1 : 2;
+        } else {
+            k = FZ_WALK_COUNT_RUNS;
+            cb = 4;
+        }
+    } else if (p->mode != FZ_COUNT && z.t > 0 && p->n >= z.ltop) {
+        k = FZ_WALK_DEEP;
+    } else if (z.L == 0) {
+        k = FZ_WALK_TABLE;
+    }
+    if (kind) *kind = k;
+    if (card_bytes) *card_bytes = cb;
+    return FZ_OK;
+}
 
 fz_status fz_plan_shard(const fz_plan *p, void *stream, uint64_t *row_begin, uint64_t *rows, uint64_t *nslices)
 {
@@ -1220,6 +1376,8 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
     if (p->mode != FZ_COUNT && z.t > 0 && p->n >= z.ltop)   // partial memo: Memo[p] missing for p >= ltop
         return launch_deep(z.d, z.t, (int)p->mode, a, m->S, z.ltop, m->off, (cudaStream_t)stream);
     if (z.L == 0) return launch_table(z.d, (int)p->mode, a, m->off, (cudaStream_t)stream);
+    if (p->mode == FZ_COUNT && p->pp.on)
+        return launch_pairs(z.d, z.t, p->pp, a, m->C, m->cardT, a.wt.R, (cudaStream_t)stream);
     return launch_walk(z.d, z.t, (int)p->mode, a, (cudaStream_t)stream);
 }
 
@@ -1259,19 +1417,101 @@ fz_status fz_enumerate(const fz_memo *m, uint64_t n, fz_mode mode, int shard, in
 }
 
 // ------------------------------------------------------------- end to end
-static constexpr int kRunChunks = 8;
+// fz_run_host (Outputs -> Buffer -> copyDeviceBufferToHostAndClear,
+// flushed whenever a buffer is full and once at the end).  The device holds the memo and a RING of
+// kRingSlots output slots; MATERIALIZE output of any size is cut into chunks of at most one slot (the
+// K4 shard cut with nshards = chunks), each chunk enumerated into its slot and copied to the host on a
+// copy stream while the next chunks are enumerated; a slot is reused once its copy has drained (events).
+// Device memory is bounded by the workspace the caller passes, not by |Z(n)|.
+}  // extern "C"
 
-fz_status fz_run_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, uint64_t *bytes)
+namespace {
+constexpr int kRingSlots = 4;
+constexpr uint64_t kRunRingDefault = 64ull << 20;   // default output ring of fz_run_workspace_bytes (4 x 16 MB)
+
+struct RunCtx {   // per-thread copy stream and ring events, created once per device (never destroyed:
+                  // a thread-exit destructor could run after the CUDA runtime's own teardown)
+    int dev = -1;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ready[kRingSlots] = {}, drained[kRingSlots] = {};
+};
+thread_local RunCtx g_run;
+
+fz_status run_ctx(RunCtx *&out)
+{
+    int dev = 0;
+    FZ_CUDA(cudaGetDevice(&dev));
+    if (g_run.dev != dev) {
+        RunCtx c;
+        c.dev = dev;
+        FZ_CUDA(cudaStreamCreateWithFlags(&c.cs, cudaStreamNonBlocking));
+        for (int i = 0; i < kRingSlots; ++i) {
+            FZ_CUDA(cudaEventCreateWithFlags(&c.ready[i], cudaEventDisableTiming));
+            FZ_CUDA(cudaEventCreateWithFlags(&c.drained[i], cudaEventDisableTiming));
+        }
+        g_run = c;   // (a context of an earlier device is left alive: its device may be used again)
+    }
+    out = &g_run;
+    return FZ_OK;
+}
+
+// the layout of the last fz_run_host call of this thread (A1 host tables reused across identical calls)
+struct RunLayoutCache {
+    uint32_t g[FZ_MAX_D] = {0};
+    int d = -1, t = -1, with_entries = -1;
+    uint64_t n = 0, cap = 0;
+    int fill = 0;
+    fz_layout *lay = nullptr;
+};
+thread_local RunLayoutCache g_run_lay;
+
+fz_status run_layout(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, const fz_layout *&out)
+{
+    if (!gens || d < 1 || d > FZ_MAX_D) return fail(FZ_EINVAL, "gens NULL or d=%d outside [1, %d]", d, FZ_MAX_D);
+    RunLayoutCache &c = g_run_lay;
+    const int we = mode != FZ_COUNT;
+    bool hit = c.lay && c.d == d && c.t == t && c.n == n && c.with_entries == we && c.cap == g_memo_cap.load() &&
+               c.fill == g_fill_override.load();
+    for (int i = 0; hit && i < d; ++i) hit = c.g[i] == gens[i];
+    if (!hit) {
+        fz_layout *lay = nullptr;
+        fz_status st = make_layout(gens, d, t, n + 1, we, &lay, FZ_MEMO_TOP_AUTO);
+        if (st) return st;
+        delete c.lay;
+        c.lay = lay;
+        for (int i = 0; i < d; ++i) c.g[i] = gens[i];
+        c.d = d;
+        c.t = t;
+        c.n = n;
+        c.with_entries = we;
+        c.cap = g_memo_cap.load();
+        c.fill = g_fill_override.load();
+    }
+    out = c.lay;
+    return FZ_OK;
+}
+
+constexpr uint64_t kRunFixed = kPlanHeader * kRingSlots + 256;   // plan headers + the run accumulator
+}  // namespace
+
+extern "C" {
+
+fz_status fz_run_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mode, uint64_t ring_bytes,
+                                 uint64_t *bytes)
 {
     if (!bytes) return fail(FZ_EINVAL, "bytes is NULL");
-    fz_layout *lay = nullptr;
-    fz_status st = make_layout(gens, d, t, n + 1, mode != FZ_COUNT, &lay, FZ_MEMO_TOP_AUTO);
+    if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode");
+    const fz_layout *lay = nullptr;
+    fz_status st = run_layout(gens, d, t, n, mode, lay);
     if (st) return st;
-    const uint64_t rows = lay->H.S[n];
-    const int chunks = (mode == FZ_MATERIALIZE) ? kRunChunks : 1;
-    uint64_t out_b = (mode == FZ_MATERIALIZE) ? align_up(rows * 4ull * d, 256) : 0;
-    *bytes = align_up(lay->z.lay.total, 256) + plan_bytes() * chunks + out_b;
-    delete lay;
+    uint64_t ring = 0;
+    if (mode == FZ_MATERIALIZE) {   // the ring asked for, else what the output needs, at most kRunRingDefault
+        const uint64_t out_b = lay->H.S[n] * 4ull * d;
+        ring = ring_bytes ? ring_bytes
+                          : std::min<uint64_t>(kRunRingDefault, align_up(out_b, 256) + kRingSlots * 256ull);
+        ring = std::max<uint64_t>(ring, kRingSlots * align_up(32ull * 4 * d, 256));   // >= 32 rows per slot
+    }
+    *bytes = align_up(lay->z.lay.total, 256) + kRunFixed + ring;
     return FZ_OK;
 }
 
@@ -1280,73 +1520,79 @@ fz_status fz_run_host(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mo
                       uint64_t *hash_out)
 {
     if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode");
-    fz_layout *lay = nullptr;
-    fz_status st = make_layout(gens, d, t, n + 1, mode != FZ_COUNT, &lay, FZ_MEMO_TOP_AUTO);
+    if (!d_ws || ((uintptr_t)d_ws & 255)) return fail(FZ_EINVAL, "workspace NULL or not 256-byte aligned");
+    const fz_layout *lay = nullptr;
+    fz_status st = run_layout(gens, d, t, n, mode, lay);
     if (st) return st;
     const uint64_t rows_total = lay->H.S[n];
-    const int chunks = (mode == FZ_MATERIALIZE) ? kRunChunks : 1;
     const uint64_t memo_b = align_up(lay->z.lay.total, 256);
-    const uint64_t need = memo_b + plan_bytes() * chunks +
-                          ((mode == FZ_MATERIALIZE) ? align_up(rows_total * 4ull * d, 256) : 0);
-    if (ws_bytes < need) {
-        delete lay;
-        return fail(FZ_ENOSPC, "workspace %llu B < %llu B", (unsigned long long)ws_bytes, (unsigned long long)need);
+    if (ws_bytes < memo_b + kRunFixed)
+        return fail(FZ_ENOSPC, "workspace %llu B < %llu B (memo + plan headers)", (unsigned long long)ws_bytes,
+                    (unsigned long long)(memo_b + kRunFixed));
+    // output ring: whatever the workspace holds beyond the memo and the headers, in kRingSlots slots
+    const uint64_t slot_b = ((ws_bytes - memo_b - kRunFixed) / kRingSlots) & ~255ull;
+    const uint64_t slot_rows = slot_b / (4ull * d);
+    if (mode == FZ_MATERIALIZE) {
+        if (rows_total && slot_rows == 0)
+            return fail(FZ_ENOSPC, "workspace leaves no room for an output ring (%llu B per slot)",
+                        (unsigned long long)slot_b);
+        if (rows_total && (!h_out || h_out_capacity_rows < rows_total))
+            return fail(FZ_ENOSPC, "host output holds %llu rows, |Z(n)| = %llu",
+                        (unsigned long long)h_out_capacity_rows, (unsigned long long)rows_total);
     }
-    if (mode == FZ_MATERIALIZE && (!h_out || h_out_capacity_rows < rows_total)) {
-        delete lay;
-        return fail(FZ_ENOSPC, "host output holds %llu rows, |Z(n)| = %llu", (unsigned long long)h_out_capacity_rows,
-                    (unsigned long long)rows_total);
-    }
+    RunCtx *rc = nullptr;
+    if ((st = run_ctx(rc))) return st;
     char *w = (char *)d_ws;
     cudaStream_t s = (cudaStream_t)stream;
-    fz_memo *m = nullptr;
-    if ((st = fz_memo_build_layout(lay, w, memo_b, stream, &m))) {
-        delete lay;
-        return st;
-    }
-    m->owned = lay;
     char *plan_area = w + memo_b;
-    uint32_t *d_out = (uint32_t *)(plan_area + plan_bytes() * chunks);
-    cudaStream_t cs = nullptr;
-    std::vector<cudaEvent_t> ev(chunks, nullptr);
-    if (mode == FZ_MATERIALIZE) {
-        FZ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        for (auto &e : ev) FZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    uint64_t tot_rows = 0, tot_hash = 0;
-    std::vector<fz_plan *> plans(chunks, nullptr);
-    for (int c = 0; c < chunks && !st; ++c) {
-        st = fz_plan_create(m, n, mode, c, chunks, plan_area + plan_bytes() * c, plan_bytes(), stream, &plans[c]);
+    uint64_t *acc = (uint64_t *)(plan_area + kPlanHeader * kRingSlots);
+    char *ring = plan_area + kRunFixed;
+    FZ_CUDA(cudaMemsetAsync(acc, 0, 3 * sizeof(uint64_t), s));
+    fz_memo *m = nullptr;
+    if ((st = fz_memo_build_layout(lay, w, memo_b, stream, &m))) return st;
+    const uint64_t nch = (mode == FZ_MATERIALIZE && rows_total) ? (rows_total + slot_rows - 1) / slot_rows : 1;
+    for (uint64_t c = 0; c < nch && !st; ++c) {
+        const int slot = (int)(c % kRingSlots);
+        if (mode == FZ_MATERIALIZE && c >= (uint64_t)kRingSlots &&
+            cudaStreamWaitEvent(s, rc->drained[slot], 0) != cudaSuccess) {   // the slot's last copy drained
+            st = cuda_check("ring slot wait");
+            break;
+        }
+        fz_plan *p = nullptr;
+        st = fz_plan_create(m, n, mode, (int)c, (int)nch, plan_area + kPlanHeader * slot, kPlanHeader, stream, &p);
         if (st) break;
-        uint64_t rb = 0, rl = 0;
-        host_shard(lay, n, mode, chunks, c, rb, rl);
-        st = fz_enumerate_launch(plans[c], d_out + rb * (uint64_t)d, rows_total - rb, ~0ull, stream);
+        uint32_t *d_slot = (uint32_t *)(ring + (uint64_t)slot * slot_b);
+        st = fz_enumerate_launch(p, mode == FZ_MATERIALIZE ? d_slot : nullptr,
+                                 mode == FZ_MATERIALIZE ? slot_rows : 0, ~0ull, stream);
+        fz_plan_free(p);
         if (st) break;
-        if (mode == FZ_MATERIALIZE && rl) {
-            if (cudaEventRecord(ev[c], s) != cudaSuccess || cudaStreamWaitEvent(cs, ev[c], 0) != cudaSuccess ||
-                cudaMemcpyAsync(h_out + rb * (uint64_t)d, d_out + rb * (uint64_t)d, rl * 4ull * d,
-                                cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+        fzk::k_run_acc<<<1, 32, 0, s>>>((const PlanHdr *)(plan_area + kPlanHeader * slot), acc);
+        ++g_launches;
+        if ((st = cuda_check("k_run_acc"))) break;
+        if (mode == FZ_MATERIALIZE) {   // chunk c = rows [rb, rb + rl) of the K4 cut (the host twin of it)
+            uint64_t rb = 0, rl = 0;
+            host_shard(lay, n, mode, (int)nch, (int)c, rb, rl, nullptr);
+            if (rl && (cudaEventRecord(rc->ready[slot], s) != cudaSuccess ||
+                       cudaStreamWaitEvent(rc->cs, rc->ready[slot], 0) != cudaSuccess ||
+                       cudaMemcpyAsync(h_out + rb * (uint64_t)d, d_slot, rl * 4ull * d, cudaMemcpyDeviceToHost,
+                                       rc->cs) != cudaSuccess ||
+                       cudaEventRecord(rc->drained[slot], rc->cs) != cudaSuccess))
                 st = cuda_check("chunk D2H");
         }
     }
-    for (int c = 0; c < chunks && !st; ++c) {
-        uint64_t r = 0, h = 0;
-        st = fz_plan_result(plans[c], stream, &r, &h);
-        tot_rows += r;
-        tot_hash += h;
+    uint64_t res[3] = {0, 0, 0};
+    {   // drain both streams whatever happened (nothing may still reference the workspace), then read
+        const cudaError_t e1 = cudaStreamSynchronize(rc->cs), e0 = cudaStreamSynchronize(s);
+        if (!st && (e0 != cudaSuccess || e1 != cudaSuccess))
+            st = fail(FZ_ECUDA, "run streams: %s", cudaGetErrorString(e0 != cudaSuccess ? e0 : e1));
+        if (!st && cudaMemcpy(res, acc, sizeof res, cudaMemcpyDeviceToHost) != cudaSuccess)
+            st = cuda_check("result read");
     }
-    if (cs) {
-        cudaError_t e = cudaStreamSynchronize(cs);
-        if (!st && e != cudaSuccess) st = fail(FZ_ECUDA, "D2H stream: %s", cudaGetErrorString(e));
-        cudaStreamDestroy(cs);
-    }
-    for (auto &e : ev)
-        if (e) cudaEventDestroy(e);
-    for (auto *p : plans) fz_plan_free(p);
     fz_free(m);
     if (st) return st;
-    if (rows_out) *rows_out = tot_rows;
-    if (hash_out) *hash_out = tot_hash;
+    if (res[2]) return fail(FZ_ENOSPC, "an output chunk overflowed its ring slot");
+    if (rows_out) *rows_out = res[0];
+    if (hash_out) *hash_out = res[1];
     return FZ_OK;
 }
 

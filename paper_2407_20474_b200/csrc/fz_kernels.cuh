@@ -60,6 +60,8 @@ struct PlanHdr {
     uint64_t row_begin;    // global row index of the shard's first row
     uint64_t rows;         // rows of Z(n) in this shard
     unsigned long long next_slice;   // K5 work queue (slices are claimed with atomicAdd)
+    uint64_t gss_warps;    // != 0: guided slices (COUNT pair walk): rounds of gss_warps slices, each round
+                           // half the size of the last, down to slice_len (gss_begin); 0: uniform slices
 };
 static_assert(sizeof(PlanHdr) <= 256, "plan header");
 
@@ -69,9 +71,43 @@ struct PlanArgs {
     uint64_t max_slices;
     uint64_t floor_len;
     int mode, shard, nshards, L;
-    int cut_given;       // COUNT: the shard's unit range [ub, ue) comes from the host's cost-balanced cut
-    uint64_t ub, ue;
+    int pairs;           // COUNT pair walk: units are cost ranks of the C tables, cut at outer prefixes
+    uint64_t wg;         // pair walk: warps of the K5 grid (guided slice rounds)
+    uint64_t gss_tail;   // pair walk: the last slices are ~ 1/gss_tail of a warp's share
 };
+
+// Guided slices (pair walk): round r has `wg` slices of (len >> (r + 1)) / wg units each, until that
+// size drops to `fl`; the rest is cut into slices of fl units.  First unit of slice i (clamped to len).
+__host__ __device__ __forceinline__ uint64_t gss_begin(uint64_t i, uint64_t len, uint64_t wg, uint64_t fl)
+{
+    uint64_t B = 0;
+    for (int r = 0; r < 63; ++r) {
+        const uint64_t z = (len >> (r + 1)) / wg;
+        if (z <= fl) {
+            B += i * fl;
+            break;
+        }
+        if (i < wg) {
+            B += i * z;
+            break;
+        }
+        B += wg * z;
+        i -= wg;
+    }
+    return B < len ? B : len;
+}
+
+__host__ __device__ __forceinline__ uint64_t gss_count(uint64_t len, uint64_t wg, uint64_t fl)
+{
+    uint64_t B = 0, ns = 0;
+    for (int r = 0; r < 63; ++r) {
+        const uint64_t z = (len >> (r + 1)) / wg;
+        if (z <= fl) return ns + (len - B + fl - 1) / fl;
+        B += wg * z;
+        ns += wg;
+    }
+    return ns;
+}
 
 // x / g for x < 2^32 by the precomputed magic M = ceil(2^64 / g) (M = 0 encodes g = 1): the error of
 // x M / 2^64 against x / g is below x / 2^64 < 1 / g, so the floor is exact.
@@ -130,6 +166,9 @@ struct Tables {
     uint32_t *rows;     // memo rows (the last tail level is written by K2 stage B), or nullptr
     uint8_t lg_a[kMaxD], lg_b[kMaxD];   // fill mode 5: log2 lanes per x of the chain-list / block passes, per level
     uint64_t *trace;    // diagnostics: per-CTA phase timestamps [grid][16][2] (FZ_K1_TRACE), or nullptr
+    uint64_t *C;        // COUNT cost tables C_0..C_{L-3} ((L-2) x top, L >= 3), or nullptr
+    uint64_t beta;      // COUNT cost of one innermost run beyond its card lookups
+    uint64_t gamma;     // COUNT cost of one outer prefix beyond its runs
 };
 
 // ------------------------------------------------------------------ helpers
@@ -921,10 +960,11 @@ __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigne
     if (lastW > last) last = lastW;
     // column-scan CTAs of phase p (leading CTAs); the rest of the grid does the other work of p
     auto ncols = [&](int p) -> uint64_t {
-        const int i = d - 3 - p, j = L - 2 - p;
+        const int i = d - 3 - p, j = L - 2 - p, jc = L - 2 - p;
         uint64_t c = 0;
         if (p >= 0 && i >= 0) c += G.g[i] < top ? G.g[i] : top;
         if (p >= 0 && j >= 0) c += G.g[j] < top ? G.g[j] : top;
+        if (tb.C && p >= 1 && jc >= 0) c += G.g[jc] < top ? G.g[jc] : top;
         return c;
     };
     auto free0 = [&](int p) -> uint32_t {   // first CTA free of column scans in phase p (0: share the grid)
@@ -959,8 +999,25 @@ __device__ __forceinline__ void k1_body(const Gens &G, const Tables &tb, unsigne
             const uint64_t gj = j >= 0 ? G.g[j] : 1;
             const uint64_t ncolW = j >= 0 ? (gj < top ? gj : top) : 0;
             const uint64_t gw1 = L >= 1 ? G.g[L - 1] : 1;
-            for (uint64_t c = blockIdx.x; c < ncolS + ncolW; c += gridDim.x) {
-                if (c < ncolS) {
+            // COUNT cost tables (pair walk): C_{L-2}[x] = W_{L-2}[x] + beta (x / g_{L-2} + 1) + gamma
+            // (each innermost run costs its lookups plus beta, each outer prefix gamma more), C_jc = column scan
+            // of C_{jc+1} by g_jc,
+            // one phase behind W (C_{L-3} in phase 1 reads the W_{L-2} of phase 0)
+            const int jc = L - 2 - p;
+            const uint64_t gc = (tb.C && p >= 1 && jc >= 0) ? G.g[jc] : 1;
+            const uint64_t ncolC = (tb.C && p >= 1 && jc >= 0) ? (gc < top ? gc : top) : 0;
+            for (uint64_t c = blockIdx.x; c < ncolS + ncolW + ncolC; c += gridDim.x) {
+                if (c >= ncolS + ncolW) {
+                    uint64_t *dst = tb.C + (uint64_t)jc * top;
+                    if (jc + 1 == L - 2) {
+                        const uint64_t *W2 = tb.W + (uint64_t)(L - 2) * top;
+                        const uint64_t g2 = G.g[L - 2], beta = tb.beta, gamma = tb.gamma;
+                        block_column_scan_w([=](uint64_t x) { return __ldcg(W2 + x) + beta * (x / g2 + 1) + gamma; },
+                                            dst, top, gc, c - ncolS - ncolW, sm);
+                    } else {
+                        block_column_scan(tb.C + (uint64_t)(jc + 1) * top, dst, top, gc, c - ncolS - ncolW, sm);
+                    }
+                } else if (c < ncolS) {
                     uint64_t *dst = tb.S + (uint64_t)i * top;
                     if (p == 0)
                         block_column_scan_w([&](uint64_t x) { return prog_count(tb.P, (uint32_t)x); }, dst, top, gi,
@@ -1266,27 +1323,72 @@ __device__ uint64_t row_rank(const uint64_t *__restrict__ S, uint64_t top, const
     return R;
 }
 
+// nextCandidate over the first nl coordinates: the rightmost nonzero a_i, i < nl,
+// decrements and the later ones restart at their maximum r_j / g_j; false at the end of the stream.
+__device__ __forceinline__ bool prefix_next(uint32_t *a, const Gens &G, int nl, uint64_t n)
+{
+    int i = -1;
+    for (int j = 0; j < nl; ++j)
+        if (a[j] > 0) i = j;
+    if (i < 0) return false;
+    uint64_t r = n;
+    for (int j = 0; j < nl; ++j) {
+        if (j == i) a[j] -= 1;
+        if (j > i) a[j] = (uint32_t)(r / G.g[j]);
+        r -= (uint64_t)a[j] * G.g[j];
+    }
+    return true;
+}
+
+// Pair walk (COUNT, L >= 3): the global row of the first outer prefix (a_1..a_{L-2}) whose first cost
+// rank is >= u (an outer prefix belongs to the shard / slice holding its first cost rank); the C
+// tables C_0..C_{L-3} rank outer prefixes by cost.  rows_total when there is none.
+__device__ uint64_t pair_row_at(const uint64_t *__restrict__ C, const uint64_t *__restrict__ S, uint64_t top,
+                                const Gens &G, int L, uint64_t n, uint64_t u, uint64_t U, uint64_t rows_total)
+{
+    if (u >= U) return rows_total;
+    uint32_t a[kMaxD];
+    for (int j = 0; j < kMaxD; ++j) a[j] = 0;
+    const uint64_t rin = unrank(C, top, G, L - 2, n, u, a);
+    if (rin > 0 && !prefix_next(a, G, L - 2, n)) return rows_total;
+    return row_rank(S, top, G, L - 2, n, a);
+}
+
 // K4: shard geometry, entirely on the device (no host round trip).  One warp.
-// MAT/HASH cut the rows of Z(n) evenly; COUNT cuts the leading-prefix walk evenly.
-// The slices themselves are unranked by the K5 warp that walks them.
+// MAT/HASH cut the rows of Z(n) evenly; COUNT cuts the leading-prefix walk evenly, or, for the pair
+// walk, the cost ranks of the C tables (each outer prefix goes whole to the shard holding its first
+// cost rank).  The slices themselves are unranked by the K5 warp that walks them.
 __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t *__restrict__ S,
-                                               const uint64_t *__restrict__ W, PlanHdr *hdr)
+                                               const uint64_t *__restrict__ W, const uint64_t *__restrict__ C,
+                                               PlanHdr *hdr)
 {
     griddep_wait();   // PDL: the count tables of the memo build are complete and visible
     griddep_launch();
     const int lane = threadIdx.x & 31;
     const bool count_mode = (A.mode == FZ_COUNT) && A.L > 0;   // t = d (L = 0): rows in every mode
-    const uint64_t *Tb = count_mode ? W : S;
+    const uint64_t *Tb = A.pairs ? C : (count_mode ? W : S);
     const uint64_t U = __ldg(Tb + A.n);
-    const uint64_t ub = A.cut_given ? A.ub : mul_div(U, A.shard, A.nshards);
-    const uint64_t ue = A.cut_given ? A.ue : mul_div(U, A.shard + 1, A.nshards);
+    const uint64_t ub = mul_div(U, A.shard, A.nshards);
+    const uint64_t ue = mul_div(U, A.shard + 1, A.nshards);
     const uint64_t len = ue - ub;
-    uint64_t slice_len = (len + A.max_slices - 1) / A.max_slices;
-    if (slice_len < A.floor_len) slice_len = A.floor_len;
-    if (slice_len > (1ull << 31)) slice_len = 1ull << 31;   // K5 COUNT keeps the budget in 32 bits
-    const uint64_t nslices = (len + slice_len - 1) / slice_len;
+    uint64_t slice_len, nslices, gw = 0;
+    if (A.pairs) {
+        gw = A.wg;
+        slice_len = len / (A.wg * A.gss_tail);
+        if (slice_len < 1024) slice_len = 1024;
+        nslices = gss_count(len, gw, slice_len);
+    } else {
+        slice_len = (len + A.max_slices - 1) / A.max_slices;
+        if (slice_len < A.floor_len) slice_len = A.floor_len;
+        if (slice_len > (1ull << 26)) slice_len = 1ull << 26;   // K5 sums 32 lanes' budgets in 32 bits
+        nslices = (len + slice_len - 1) / slice_len;
+    }
     uint64_t rb = ub, re = ue;
-    if (count_mode) {
+    if (A.pairs) {
+        const uint64_t rows_total = __ldg(S + A.n);
+        rb = pair_row_at(C, S, A.top, G, A.L, A.n, ub, U, rows_total);
+        re = pair_row_at(C, S, A.top, G, A.L, A.n, ue, U, rows_total);
+    } else if (count_mode) {
         const uint64_t rows_total = __ldg(S + A.n);
         uint32_t a[kMaxD];
         for (int j = 0; j < kMaxD; ++j) a[j] = 0;
@@ -1316,6 +1418,7 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
         h.row_begin = rb;
         h.rows = re - rb;
         h.next_slice = 0;
+        h.gss_warps = gw;
         *hdr = h;
     }
 }
@@ -1377,6 +1480,17 @@ __device__ __forceinline__ void store_row(uint32_t *p, const uint32_t (&w)[D])
     }
 }
 
+__device__ __forceinline__ void st_cs_u32(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_cs_v4(uint32_t *p, const uint4 &v)
+{
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 struct BlockInfo {      // one non-empty memo block of the current warp round (16 B)
     uint64_t memo_row;  // first memo row to copy (off[p] + k offset)
     uint32_t start;     // first output row of the block, relative to the round
@@ -1399,51 +1513,31 @@ struct WalkTables {
 };
 
 
-template <int D, int T, int MODE, bool U8 = false>
+template <int D, int T, int MODE>
 __global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : 2)))
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
                                                          uint32_t f0n, uint32_t c16R)
 {
-    constexpr bool c8 = U8;   // COUNT outer-prefix walk with u8 cards (every card < 256)
     griddep_wait();   // PDL: the plan header (K4) and the memo tables are complete and visible
     extern __shared__ uint64_t f0s[];   // level-0 unrank column (f0n entries, 0 = not cached)
     for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Tb + (n64 - (uint64_t)q * G.g[0]));
-    // COUNT: card[x] = S_L[x], x <= n, in shared memory after f0s, residue-major w.r.t. m = g_L with c16R
-    // entries per residue column (16-B aligned columns; c16R = 0: not staged); u16 entries, or u8 when c8
-    // (every card < 256, outer-prefix walk only)
+    // COUNT, L = 2: card[x] = S_L[x], x <= n, as u16 in shared memory after f0s, residue-major w.r.t.
+    // m = g_L with c16R entries per residue column (16-B aligned columns; c16R = 0: not staged)
     uint16_t *c16 = reinterpret_cast<uint16_t *>(f0s + ((f0n + 1) & ~1u));
-    uint8_t *c8t = reinterpret_cast<uint8_t *>(c16);
     if (c16R) {
         const uint32_t mm = G.g[D - T - 1];
-        for (uint32_t x = threadIdx.x; x <= (uint32_t)n64; x += blockDim.x) {
-            const uint32_t i = (x % mm) * c16R + x / mm;
-            const uint64_t c = __ldg(wt.card64 + x);
-            if (c8)
-                c8t[i] = (uint8_t)c;
-            else
-                c16[i] = (uint16_t)c;
-        }
-    }
-    // COUNT: masks keeping the first tl entries of a 16-B vector (tl = 0..7 u16 entries, 0..15 u8 entries)
-    __shared__ uint4 tailmask[MODE == FZ_COUNT ? 16 : 1];
-    if (MODE == FZ_COUNT && threadIdx.x < 16) {
-        const uint32_t tl = threadIdx.x;
-        auto w = [&](uint32_t i) {   // word i of the mask
-            if (c8) {
-                uint32_t r = 0;
-                for (uint32_t b = 0; b < 4; ++b) r |= (4 * i + b < tl) ? 0xffu << (8 * b) : 0u;
-                return r;
-            }
-            return tl > 2 * i + 1 ? 0xffffffffu : (tl > 2 * i ? 0xffffu : 0u);
-        };
-        tailmask[MODE == FZ_COUNT ? tl : 0] = make_uint4(w(0), w(1), w(2), w(3));
+        for (uint32_t x = threadIdx.x; x <= (uint32_t)n64; x += blockDim.x)
+            c16[(x % mm) * c16R + x / mm] = (uint16_t)__ldg(wt.card64 + x);
     }
     __syncthreads();
     constexpr int L = D - T;
     static_assert(L >= 1, "at least one leading coordinate");
     __shared__ BlockInfo binfo[MODE == FZ_COUNT ? 1 : kWalkThreads / 32][32];   // MAT/HASH block lists
+    // MATERIALIZE with d not a multiple of 4: per-warp staging of 128 rows as a word stream (+ 3 words of phase)
+    constexpr bool kWordStream = MODE == FZ_MATERIALIZE && (D % 4) != 0;
+    __shared__ __align__(16) uint32_t wsb[kWordStream ? kWalkThreads / 32 : 1][kWordStream ? 128 * D + 4 : 1];
     const int lane = threadIdx.x & 31, wib = (MODE == FZ_COUNT) ? 0 : threadIdx.x >> 5;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -1478,9 +1572,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
             uint32_t ua[kMaxD];
 #pragma unroll
             for (int j = 0; j < kMaxD; ++j) ua[j] = 0;
-            // the COUNT outer-prefix walk needs only the outer prefix (a_1..a_{L-2}) holding the slice start
-            const int ulev = (MODE == FZ_COUNT && L >= 3 && c16R) ? L - 2 : L;
-            const uint64_t k0 = unrank(Tb, top, G, ulev, n64, shard_begin + sl.begin, ua, f0n ? f0s : nullptr);
+            const uint64_t k0 = unrank(Tb, top, G, L, n64, shard_begin + sl.begin, ua, f0n ? f0s : nullptr);
             sl.k0 = (MODE == FZ_COUNT) ? 0 : k0;
 #pragma unroll
             for (int j = 0; j < L; ++j) sl.a[j] = ua[j];
@@ -1505,147 +1597,6 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
             // table staged in shared memory (u16, natural layout), whole runs go one per lane: lane l
             // takes sibling a_{L-2} - l and sums card[r_l - v m], v = 0..r_l / m, so the per-run
             // bookkeeping is shared by 32 runs.
-            if constexpr (L >= 3) {
-                if (c16R) {
-                    // Outer-prefix walk (staged card table, L >= 3): the slice [b, e) of leading-prefix
-                    // ranks takes exactly the outer prefixes (a_1..a_{L-2}) whose FIRST leading prefix has
-                    // its rank in [b, e) (every outer prefix in exactly one slice of one shard).  An outer
-                    // prefix with remainder R holds the runs a_{L-1} = A..0 (A = R / g_{L-1}), each the
-                    // innermost run v = rin / m .. 0 of remainder rin = R - a_{L-1} g_{L-1}; lane l sums
-                    // the runs A - l, A - l - 32, .. alone (one card lookup per leading prefix, no
-                    // per-run budget).  Ranks: the first leading prefix of an outer prefix has rank
-                    // sum_{j < L-2} W_j[r_j - (a_j + 1) g_j]; an outer prefix holds W_{L-2}[R] prefixes.
-                    const uint64_t b = shard_begin + sl.begin, e = b + sl.len;
-                    const uint32_t g2 = G.g[L - 2];
-                    const uint64_t mmag = wt.gmag[L - 1], g2mag = wt.gmag[L - 2];
-                    const uint32_t rdq = (uint32_t)((32ull * g2) / m), rdc = (uint32_t)((32ull * g2) % m);
-                    uint32_t o[L - 2], rj[L - 1];   // outer coordinates, remainders r_0 = n, r_{j+1}
-                    rj[0] = n;
-#pragma unroll
-                    for (int j = 0; j < L - 2; ++j) {
-                        o[j] = sl.a[j];
-                        rj[j + 1] = rj[j] - o[j] * G.g[j];
-                    }
-                    uint64_t ob = 0;
-#pragma unroll
-                    for (int j = 0; j < L - 2; ++j) {
-                        const uint32_t nx = (o[j] + 1) * G.g[j];
-                        if (nx <= rj[j]) ob += __ldg(Tb + (uint64_t)j * top + (rj[j] - nx));
-                    }
-                    const uint64_t *WL2 = Tb + (uint64_t)(L - 2) * top;
-                    // nextCandidate over the outer coordinates (rightmost nonzero a_i, i < L-2, decrements;
-                    // later outer coordinates restart at their maximum); false at the end of the stream
-                    auto outer_next = [&]() -> bool {
-                        int i = -1;
-#pragma unroll
-                        for (int j = 0; j < L - 2; ++j)
-                            if (o[j] > 0) i = j;
-                        if (i < 0) return false;
-#pragma unroll
-                        for (int j = 0; j < L - 2; ++j) {
-                            if (j == i) o[j] -= 1;
-                            if (j > i) o[j] = fdiv(rj[j], wt.gmag[j]);
-                            if (j >= i) rj[j + 1] = rj[j] - o[j] * G.g[j];
-                        }
-                        return true;
-                    };
-                    bool live = true;
-                    if (ob < b) {   // the outer prefix began in an earlier slice
-                        ob += __ldg(WL2 + rj[L - 2]);
-                        live = outer_next();
-                    }
-                    while (live && ob < e) {
-                        const uint32_t R = rj[L - 2];
-                        const uint64_t wR = __ldg(WL2 + R);   // prefixes of this outer prefix (used after the runs)
-                        const uint32_t A = fdiv(R, g2mag);
-                        const uint32_t rmin = R - A * g2;
-                        if (lane <= A) {
-                            // run k = lane, lane + 32, ..: remainder rl = rmin + k g2, column rl mod m with
-                            // entries 0 .. rl / m; both stepped incrementally by 32 g2 = dq m + dc
-                            const uint32_t rl = rmin + lane * g2;
-                            uint32_t qq = fdiv(rl, mmag);
-                            uint32_t cl = rl - qq * m;
-                            for (uint32_t k = lane; k <= A; k += 32) {
-                                const uint32_t len = qq + 1;
-                                uint32_t s0 = 0, s1 = 0;
-                                if constexpr (U8) {   // u8 cards: 16 per vector, 4 per dp4a
-                                    const uint4 *vp = reinterpret_cast<const uint4 *>(c8t + cl * c16R);
-                                    const uint32_t nv = len >> 4;
-                                    uint32_t kk = 0;
-#pragma unroll 1
-                                    for (; kk + 2 <= nv; kk += 2) {
-                                        const uint4 w0 = vp[kk], w1 = vp[kk + 1];
-                                        s0 = __dp4a(w0.x, 0x01010101u, s0);
-                                        s1 = __dp4a(w0.y, 0x01010101u, s1);
-                                        s0 = __dp4a(w0.z, 0x01010101u, s0);
-                                        s1 = __dp4a(w0.w, 0x01010101u, s1);
-                                        s0 = __dp4a(w1.x, 0x01010101u, s0);
-                                        s1 = __dp4a(w1.y, 0x01010101u, s1);
-                                        s0 = __dp4a(w1.z, 0x01010101u, s0);
-                                        s1 = __dp4a(w1.w, 0x01010101u, s1);
-                                    }
-                                    if (kk < nv) {   // odd full vector
-                                        const uint4 w0 = vp[kk++];
-                                        s0 = __dp4a(w0.x, 0x01010101u, s0);
-                                        s1 = __dp4a(w0.y, 0x01010101u, s1);
-                                        s0 = __dp4a(w0.z, 0x01010101u, s0);
-                                        s1 = __dp4a(w0.w, 0x01010101u, s1);
-                                    }
-                                    const uint32_t tl = len & 15;   // last partial vector: its first tl entries
-                                    if (tl) {
-                                        const uint4 w0 = vp[kk], mk = tailmask[tl];
-                                        s0 = __dp4a(w0.x & mk.x, 0x01010101u, s0);
-                                        s1 = __dp4a(w0.y & mk.y, 0x01010101u, s1);
-                                        s0 = __dp4a(w0.z & mk.z, 0x01010101u, s0);
-                                        s1 = __dp4a(w0.w & mk.w, 0x01010101u, s1);
-                                    }
-                                } else {
-                                    const uint4 *vp = reinterpret_cast<const uint4 *>(c16 + cl * c16R);
-                                    const uint32_t nv = len >> 3;
-                                    uint32_t kk = 0;
-#pragma unroll 1
-                                    for (; kk + 2 <= nv; kk += 2) {
-                                        const uint4 w0 = vp[kk], w1 = vp[kk + 1];
-                                        s0 = __dp2a_lo(w0.x, 0x0101u, s0);
-                                        s1 = __dp2a_lo(w0.y, 0x0101u, s1);
-                                        s0 = __dp2a_lo(w0.z, 0x0101u, s0);
-                                        s1 = __dp2a_lo(w0.w, 0x0101u, s1);
-                                        s0 = __dp2a_lo(w1.x, 0x0101u, s0);
-                                        s1 = __dp2a_lo(w1.y, 0x0101u, s1);
-                                        s0 = __dp2a_lo(w1.z, 0x0101u, s0);
-                                        s1 = __dp2a_lo(w1.w, 0x0101u, s1);
-                                    }
-                                    if (kk < nv) {   // odd full vector
-                                        const uint4 w0 = vp[kk++];
-                                        s0 = __dp2a_lo(w0.x, 0x0101u, s0);
-                                        s1 = __dp2a_lo(w0.y, 0x0101u, s1);
-                                        s0 = __dp2a_lo(w0.z, 0x0101u, s0);
-                                        s1 = __dp2a_lo(w0.w, 0x0101u, s1);
-                                    }
-                                    const uint32_t tl = len & 7;   // last partial vector: its first tl entries
-                                    if (tl) {
-                                        const uint4 w0 = vp[kk], mk = tailmask[tl];
-                                        s0 = __dp2a_lo(w0.x & mk.x, 0x0101u, s0);
-                                        s1 = __dp2a_lo(w0.y & mk.y, 0x0101u, s1);
-                                        s0 = __dp2a_lo(w0.z & mk.z, 0x0101u, s0);
-                                        s1 = __dp2a_lo(w0.w & mk.w, 0x0101u, s1);
-                                    }
-                                }
-                                acc_rows += s0 + s1;
-                                cl += rdc;
-                                qq += rdq;
-                                if (cl >= m) {
-                                    cl -= m;
-                                    ++qq;
-                                }
-                            }
-                        }
-                        ob += wR;
-                        live = outer_next();
-                    }
-                    continue;
-                }
-            }
             uint32_t q = r_in / m, col = r_in - q * m;
             uint32_t vv = (uint32_t)v;
             uint32_t left32 = (uint32_t)left;   // K4 keeps COUNT slices below 2^31 prefixes
@@ -1843,15 +1794,42 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                             }
                         }
                     }
-                    uint32_t *ob = out + (outpos + q0 + lane) * (uint64_t)D;   // chunk u at ob + 32 u D
+                    if constexpr (kWordStream) {
+                        // d not a multiple of 4: the warp's rows [q0, q0 + nr) are one contiguous run of nr d
+                        // words; stage them in shared memory at the 16-B phase of their global address and
+                        // write the aligned middle as 16-B vectors (scalar head and tail words)
+                        const uint32_t nr = (use - q0 < 32u * UNR) ? use - q0 : 32u * UNR;
+                        const uint64_t G0 = (outpos + q0) * (uint64_t)D;        // first word (shard-relative)
+                        const uint32_t sft = (uint32_t)(((uintptr_t)(out + G0) >> 2) & 3);
+                        uint32_t *sb = wsb[wib] + sft;
 #pragma unroll
-                    for (int u = 0; u < UNR; ++u) {
-                        if (!ok[u]) continue;
-                        const uint32_t q = q0 + 32 * u + lane;
-                        if constexpr (MODE == FZ_MATERIALIZE) {
-                            store_row<D>(ob + 32 * u * D, wv[u]);
-                        } else {
-                            acc_hash += row_hash<D>(row_base + outpos + q, wv[u]);
+                        for (int u = 0; u < UNR; ++u) {
+                            if (!ok[u]) continue;
+#pragma unroll
+                            for (int j = 0; j < D; ++j) sb[(32 * u + lane) * D + j] = wv[u][j];
+                        }
+                        __syncwarp();
+                        const uint32_t W = nr * D, head = ((4 - sft) & 3) < W ? ((4 - sft) & 3) : W;
+                        const uint32_t nv = (W - head) >> 2, tail0 = head + 4 * nv;
+                        uint32_t *og = out + G0;
+                        if ((uint32_t)lane < head) st_cs_u32(og + lane, sb[lane]);
+                        for (uint32_t v = lane; v < nv; v += 32) {
+                            const uint4 w4 = *reinterpret_cast<const uint4 *>(sb + head + 4 * v);
+                            st_cs_v4(og + head + 4 * v, w4);
+                        }
+                        if ((uint32_t)lane < W - tail0) st_cs_u32(og + tail0 + lane, sb[tail0 + lane]);
+                        __syncwarp();
+                    } else {
+                        uint32_t *ob = out + (outpos + q0 + lane) * (uint64_t)D;   // chunk u at ob + 32 u D
+#pragma unroll
+                        for (int u = 0; u < UNR; ++u) {
+                            if (!ok[u]) continue;
+                            const uint32_t q = q0 + 32 * u + lane;
+                            if constexpr (MODE == FZ_MATERIALIZE) {
+                                store_row<D>(ob + 32 * u * D, wv[u]);
+                            } else {
+                                acc_hash += row_hash<D>(row_base + outpos + q, wv[u]);
+                            }
                         }
                     }
                 }
@@ -1897,6 +1875,365 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
         acc_hash = warp_sum_u64(acc_hash);
         if (lane == 0) atomicAdd((unsigned long long *)(result + 1), (unsigned long long)acc_hash);
     }
+}
+
+// ------------------------------------------------------ K5, COUNT pair walk
+// COUNT for L >= 3 (one card lookup per leading prefix).  The walk goes
+// by OUTER prefixes o = (a_1..a_{L-2}) with remainder R (nextCandidate over the outer coordinates,
+// PAPER.md:208-218).  An outer prefix holds the runs k = 0..A, A = R / g2 (g2 = g_{L-2}); run k has
+// remainder r_k = rmin + k g2 (rmin = R - A g2) and sums card[r_k - v m], v = 0..r_k / m (m = g_{L-1}):
+// entries 0..r_k / m of the residue column r_k mod m.  One lane takes the PAIR of runs (k, A - k)
+// (k <= A / 2; k = A / 2 alone when A is even): X = run k, Y = run A - k, |X| <= |Y|, and every pass of a
+// warp fills its 32 lanes with the next 32 pairs of the outer-prefix stream, from as many outer prefixes
+// as that takes.
+//
+// Card table: staged once per CTA in shared memory as u16 (u8 when every card < 64), 16-B vectors,
+// columns of R16 entries (R16 / entries-per-vector odd).  Column order follows the runs: run k + 1 lies
+// in column (col_k + Delta) mod m, Delta = g2 mod m, so with e = gcd(Delta, m), m' = m / e the columns
+// of coset s in [0, e) are stored as the orbit s + j Delta, j = 0..m'-1, followed by `dup` (31 or 0)
+// repeated columns: the lanes of one outer prefix in a pass read consecutive stored columns (X runs
+// ascending, Y runs descending), so the 16-B vectors of 8 lanes fall in 8 distinct bank groups.  Each
+// lane reads vector j of Y and of X (while X has one) in the same iteration -- the same vector index in
+// every lane, which keeps the loads conflict-free -- adding the packed u16 (u8) words with IADD3 into two
+// packed accumulators that dp2a (dp4a) unpacks every F iterations (F = 65535 / (4 card_max), resp.
+// 255 / (4 card_max)); the masked last vector of each run is read once, its mask computed in registers.
+//
+// Slices: cost ranks of the C tables (C_{L-2}[R] = W_{L-2}[R] + beta (A + 1) + gamma: a run costs its
+// lookups plus beta, an outer prefix gamma more), guided sizes (gss_begin).  A slice [b, e) takes the
+// outer prefixes whose first cost rank lies in it: both ends are unranked through C_0..C_{L-3} (level 0
+// cached in shared memory) and the walk stops at the end's outer prefix.
+struct PairGeo {
+    uint32_t m, dlt, e, mp, dup, inv;   // m = g_{L-1}, Delta = g2 mod m, e = gcd(Delta, m), m' = m/e, inverse
+    uint32_t R16, ncolv, F;             // entries per stored column, stored columns e (m' + dup), flush period
+    uint32_t Mm, Mg2, Me, Mmp;          // div32 magics of m, g2, e, m'
+    uint32_t Mg[kMaxD];                 // div32 magics of the generators (outer carry)
+    // the common outer step (a_{L-3} decrements: R += g3, g3 = Q3 g2 + S3): column steps (mod m) and,
+    // when e = 1, orbit-position steps (mod m) for the two outcomes of rmin + S3 >= g2
+    uint32_t Q3, S3, cs1, cs2, is1, is2;
+};
+
+// x / d for any x < 2^32, d >= 1, from M = floor(2^32 / d) (d = 1: 2^32 - 1): umulhi underestimates the
+// quotient by at most one, one compare corrects it
+__device__ __forceinline__ uint32_t div32(uint32_t x, uint32_t d, uint32_t M)
+{
+    const uint32_t q = __umulhi(x, M);
+    return (x - q * d >= d) ? q + 1 : q;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
+template <bool U8>
+__device__ __forceinline__ uint32_t unpack_add(uint32_t p, uint32_t s)
+{
+    if constexpr (U8) return __dp4a(p, 0x01010101u, s);
+    else return __dp2a_lo(p, 0x0101u, s);
+}
+
+// s + the first t entries of the 16-B vector w (t < entries per vector): byte selectors of dp2a / dp4a,
+// 1 for the first t entries and 0 after (no masking of the data)
+template <bool U8>
+__device__ __forceinline__ uint32_t add_prefix(const uint4 &w, uint32_t t, uint32_t s)
+{
+    uint64_t lo, hi;
+    const uint32_t tl = U8 ? (t < 8 ? t : 8) : t, th = (U8 && t > 8) ? t - 8 : 0;
+    asm("shl.b64 %0, %1, %2;" : "=l"(lo) : "l"(~0ull), "r"(8 * tl));   // PTX clamps shifts >= 64 to 0
+    lo = ~lo & 0x0101010101010101ull;
+    if constexpr (U8) {
+        asm("shl.b64 %0, %1, %2;" : "=l"(hi) : "l"(~0ull), "r"(8 * th));
+        hi = ~hi & 0x0101010101010101ull;
+        s = __dp4a(w.x, (uint32_t)lo, s);
+        s = __dp4a(w.y, (uint32_t)(lo >> 32), s);
+        s = __dp4a(w.z, (uint32_t)hi, s);
+        s = __dp4a(w.w, (uint32_t)(hi >> 32), s);
+    } else {   // entry k of the vector <-> selector byte k: word i takes bytes 2i, 2i + 1
+        (void)hi;
+        s = __dp2a_lo(w.x, (uint32_t)lo, s);
+        s = __dp2a_hi(w.y, (uint32_t)lo, s);
+        s = __dp2a_lo(w.z, (uint32_t)(lo >> 32), s);
+        s = __dp2a_hi(w.w, (uint32_t)(lo >> 32), s);
+    }
+    return s;
+}
+
+// the outer prefix (coordinates o, remainders rj) holding cost rank u of the C tables; with its first
+// rank below u (it belongs to an earlier slice) the next one.  false: no such outer prefix.
+template <int NO>
+__device__ __forceinline__ bool pair_locate(const uint64_t *__restrict__ Ct, uint64_t top, const Gens &G,
+                                            uint64_t n64, uint64_t u, const uint64_t *F0, const PairGeo &pg,
+                                            uint32_t (&o)[NO], uint32_t (&rj)[NO + 1])
+{
+    uint32_t ua[kMaxD];
+#pragma unroll
+    for (int j = 0; j < kMaxD; ++j) ua[j] = 0;
+    const uint64_t rin = unrank(Ct, top, G, NO, n64, u, ua, F0);
+    rj[0] = (uint32_t)n64;
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+        o[j] = ua[j];
+        rj[j + 1] = rj[j] - o[j] * G.g[j];
+    }
+    if (rin == 0) return true;
+    int i = -1;
+#pragma unroll
+    for (int j = 0; j < NO; ++j)
+        if (o[j] > 0) i = j;
+    if (i < 0) return false;
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+        if (j == i) o[j] -= 1;
+        if (j > i) o[j] = div32(rj[j], G.g[j], pg.Mg[j]);
+        if (j >= i) rj[j + 1] = rj[j] - o[j] * G.g[j];
+    }
+    return true;
+}
+
+template <int D, int T, bool U8>
+__global__ void __launch_bounds__(kCountThreads, 1)
+k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uint64_t top,
+         const uint32_t *__restrict__ cardT, uint64_t Rcol, PairGeo pg, uint32_t f0n)
+{
+    constexpr int L = D - T;
+    static_assert(L >= 3, "pair walk: at least one outer coordinate");
+    constexpr int NO = L - 2;   // outer coordinates
+    constexpr uint32_t VE = U8 ? 16 : 8, VSH = U8 ? 4 : 3;   // entries per vector, log2
+    griddep_wait();   // PDL: the plan header (K4) and the count tables are complete and visible
+    extern __shared__ uint64_t f0s[];   // level-0 unrank column C_0[n - q g_0] (f0n entries), then the card image
+    for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Ct + (n64 - (uint64_t)q * G.g[0]));
+    uint8_t *img = reinterpret_cast<uint8_t *>(f0s + ((f0n + 1) & ~1u));
+    const uint32_t m = pg.m;
+    {   // stage the card image: stored column vp = coset s, orbit position j -> column (s + (j mod m') Delta) mod m
+        const uint32_t tot = pg.ncolv * pg.R16, per = pg.mp + pg.dup;
+        for (uint32_t i0 = threadIdx.x; i0 < tot; i0 += 8 * blockDim.x) {
+            uint32_t val[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t i = i0 + k * blockDim.x;
+                val[k] = 0;
+                if (i < tot) {
+                    const uint32_t vp = i / pg.R16, v = i - vp * pg.R16;
+                    const uint32_t cs = vp / per, j = (vp - cs * per) % pg.mp;
+                    const uint32_t col = (cs + j * pg.dlt) % m;
+                    if ((uint64_t)col + (uint64_t)v * m <= n64) val[k] = __ldg(cardT + (uint64_t)col * Rcol + v);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t i = i0 + k * blockDim.x;
+                if (i < tot) {
+                    if constexpr (U8) img[i] = (uint8_t)val[k];
+                    else reinterpret_cast<uint16_t *>(img)[i] = (uint16_t)val[k];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t g2 = G.g[L - 2];
+    const uint64_t shard_begin = hdr->shard_begin, shard_len = hdr->shard_len, nslices = hdr->nslices,
+                   gw = hdr->gss_warps, fl = hdr->slice_len, total = hdr->total_units;
+    const uint32_t per = pg.mp + pg.dup;
+    const uint32_t colB = pg.R16 * (U8 ? 1u : 2u);   // bytes per stored column
+    const uint32_t img_a = smem_addr(img);
+    const uint64_t *F0 = f0n ? f0s : nullptr;
+    const bool e1 = pg.e == 1;
+    uint64_t acc = 0;
+
+    for (;;) {
+        uint64_t si = 0;
+        if (lane == 0) si = atomicAdd(&hdr->next_slice, 1ull);
+        si = shfl_u64(si, 0);
+        if (si >= nslices) break;
+        const uint64_t b = shard_begin + gss_begin(si, shard_len, gw, fl),
+                       e = shard_begin + gss_begin(si + 1, shard_len, gw, fl);
+        if (b >= e) continue;
+        uint32_t o[NO], rj[NO + 1], oe[NO], re[NO + 1];
+        if (!pair_locate<NO>(Ct, top, G, n64, b, F0, pg, o, rj)) continue;
+        // the slice ends at the outer prefix holding rank e (exclusive), or at the end of the stream
+        const bool to_stream_end = e >= total || !pair_locate<NO>(Ct, top, G, n64, e, F0, pg, oe, re);
+        auto at_end = [&]() -> bool {
+            if (to_stream_end) return false;
+            bool eq = true;
+#pragma unroll
+            for (int j = 0; j < NO; ++j) eq = eq && (o[j] == oe[j]);
+            return eq;
+        };
+        if (at_end()) continue;   // the slice holds no outer prefix start
+        // the current outer prefix (uniform): remainder R, runs - 1 A, smallest run remainder rmin, column of
+        // run 0 col, its coset base cb = s (m' + dup), orbit position idx0; c = its next pair
+        uint32_t R = 0, A = 0, rmin = 0, col = 0, cb = 0, idx0 = 0, c = 0;
+        auto orbit = [&]() {   // coset and orbit position of col (e > 1)
+            const uint32_t s = col - div32(col, pg.e, pg.Me) * pg.e;
+            const uint32_t cp = div32(col - s, pg.e, pg.Me) * pg.inv;   // < m'^2
+            idx0 = cp - div32(cp, pg.mp, pg.Mmp) * pg.mp;
+            cb = s * per;
+        };
+        auto load = [&]() {
+            R = rj[NO];
+            A = div32(R, g2, pg.Mg2);
+            rmin = R - A * g2;
+            col = rmin - div32(rmin, m, pg.Mm) * m;
+            if (e1) {
+                const uint32_t cp = col * pg.inv;   // < m^2
+                idx0 = cp - div32(cp, m, pg.Mm) * m;
+                cb = 0;
+            } else {
+                orbit();
+            }
+            c = 0;
+        };
+        // nextCandidate over the outer coordinates; false at the end of the stream or the
+        // slice.  The common step (only a_{L-3} decrements, R += g3) updates R, A, rmin, col, idx0 without
+        // division.
+        auto advance = [&]() -> bool {
+            int i = -1;
+#pragma unroll
+            for (int j = 0; j < NO; ++j)
+                if (o[j] > 0) i = j;
+            if (i < 0) return false;
+            if (i == NO - 1) {
+                o[NO - 1] -= 1;
+                rj[NO] += G.g[NO - 1];
+                if (at_end()) return false;
+                R = rj[NO];
+                rmin += pg.S3;
+                A += pg.Q3;
+                const bool cy = rmin >= g2;
+                if (cy) {
+                    rmin -= g2;
+                    A += 1;
+                }
+                col += cy ? pg.cs2 : pg.cs1;
+                if (col >= m) col -= m;
+                if (e1) {
+                    idx0 += cy ? pg.is2 : pg.is1;
+                    if (idx0 >= m) idx0 -= m;
+                } else {
+                    orbit();
+                }
+                c = 0;
+                return true;
+            }
+#pragma unroll
+            for (int j = 0; j < NO; ++j) {
+                if (j == i) o[j] -= 1;
+                if (j > i) o[j] = div32(rj[j], G.g[j], pg.Mg[j]);
+                if (j >= i) rj[j + 1] = rj[j] - o[j] * G.g[j];
+            }
+            if (at_end()) return false;
+            load();
+            return true;
+        };
+        load();
+        bool live = true;
+        while (live) {
+            // fill the 32 lanes with the next pairs of the stream (as many outer prefixes as it takes)
+            uint32_t mR = 0, mA = 0, mrmin = 0, mcb = 0, mbx = 0, mby = 0, mpp = 0, mf = 0;
+            bool mine = false;
+            uint32_t filled = 0;
+            while (filled < 32 && live) {
+                const uint32_t P = A / 2 + 1;
+                const uint32_t take = (P - c < 32 - filled) ? P - c : 32 - filled;
+                if ((uint32_t)lane >= filled && (uint32_t)lane < filled + take) {
+                    mine = true;
+                    mR = R;
+                    mA = A;
+                    mrmin = rmin;
+                    mcb = cb;
+                    mbx = idx0 + c;
+                    mby = idx0 + A + 32 * pg.mp - c - 31;
+                    mpp = c;
+                    mf = filled;
+                }
+                filled += take;
+                c += take;
+                if (c == P) live = advance();
+            }
+            // this lane's pair: X = run pp (ascending stored columns), Y = run A - pp (descending, |Y| >= |X|)
+            uint32_t lenX = 0, lenY = 0, jX = 0, jY = 0;
+            if (mine) {
+                const uint32_t li = (uint32_t)lane - mf, pp = mpp + li;
+                lenX = (2 * pp == mA) ? 0u : div32(mrmin + pp * g2, m, pg.Mm) + 1;
+                lenY = div32(mR - pp * g2, m, pg.Mm) + 1;
+                if (pg.dup) {   // 32 consecutive stored columns per group, ascending / descending
+                    jX = mbx - div32(mbx, pg.mp, pg.Mmp) * pg.mp + li;
+                    jY = mby - div32(mby, pg.mp, pg.Mmp) * pg.mp + 31 - li;
+                } else {
+                    const uint32_t x = mbx + li, y = mby + 31 - li;
+                    jX = x - div32(x, pg.mp, pg.Mmp) * pg.mp;
+                    jY = y - div32(y, pg.mp, pg.Mmp) * pg.mp;
+                }
+            }
+            uint32_t xa = img_a + (mcb + jX) * colB, ya = img_a + (mcb + jY) * colB;
+            const uint32_t NX = lenX >> VSH, NY = lenY >> VSH;
+            // vector j of Y and of X (while X has one) in the same iteration: every lane reads vector index j
+            // of its columns, so the 8 lanes of a quarter-warp stay in distinct bank groups
+            uint32_t sum = 0, j = 0;
+            while (j < NY) {
+                const uint32_t je = (NY - j < pg.F) ? NY : j + pg.F;
+                uint32_t a0 = 0, a1 = 0;
+#pragma unroll 1
+                for (; j + 4 <= je; j += 4) {
+                    const uint4 y0 = lds128(ya), y1 = lds128(ya + 16), y2 = lds128(ya + 32), y3 = lds128(ya + 48);
+                    a0 += y0.x + y0.y;
+                    a1 += y0.z + y0.w;
+                    a0 += y1.x + y1.y;
+                    a1 += y1.z + y1.w;
+                    a0 += y2.x + y2.y;
+                    a1 += y2.z + y2.w;
+                    a0 += y3.x + y3.y;
+                    a1 += y3.z + y3.w;
+                    if (j < NX) {
+                        const uint4 x0 = lds128(xa);
+                        a0 += x0.x + x0.y;
+                        a1 += x0.z + x0.w;
+                    }
+                    if (j + 1 < NX) {
+                        const uint4 x1 = lds128(xa + 16);
+                        a0 += x1.x + x1.y;
+                        a1 += x1.z + x1.w;
+                    }
+                    if (j + 2 < NX) {
+                        const uint4 x2 = lds128(xa + 32);
+                        a0 += x2.x + x2.y;
+                        a1 += x2.z + x2.w;
+                    }
+                    if (j + 3 < NX) {
+                        const uint4 x3 = lds128(xa + 48);
+                        a0 += x3.x + x3.y;
+                        a1 += x3.z + x3.w;
+                    }
+                    ya += 64;
+                    xa += 64;
+                }
+#pragma unroll 1
+                for (; j < je; ++j) {
+                    const uint4 y0 = lds128(ya);
+                    a0 += y0.x + y0.y;
+                    a1 += y0.z + y0.w;
+                    if (j < NX) {
+                        const uint4 x0 = lds128(xa);
+                        a0 += x0.x + x0.y;
+                        a1 += x0.z + x0.w;
+                    }
+                    ya += 16;
+                    xa += 16;
+                }
+                sum = unpack_add<U8>(a1, unpack_add<U8>(a0, sum));
+            }
+            // the last, partial vectors (each read once; ya points at Y's vector NY, xa at X's vector NY)
+            const uint32_t tX = lenX & (VE - 1), tY = lenY & (VE - 1);
+            if (tY) sum = add_prefix<U8>(lds128(ya), tY, sum);
+            if (tX) sum = add_prefix<U8>(lds128(xa - 16 * (NY - NX)), tX, sum);
+            acc += sum;
+        }
+    }
+    acc = warp_sum_u64(acc);
+    if (lane == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)acc);
 }
 
 // ------------------------------------------------- K5, partial memo (f2)
@@ -2035,8 +2372,12 @@ __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, Pl
             }
             const unsigned dball = __ballot_sync(kFull, !leaf && cnt > 0);
             const int dl = dball ? __ffs(dball) - 1 : 32;
-            uint32_t c = (leaf && lane < dl) ? (uint32_t)cnt : 0u;
-            if (lane == 0) c -= (uint32_t)kfirst;
+            // rows this lane's leaf offers, clamped to the slice's budget (K4 keeps slices <= 2^26 rows), so
+            // the 32-lane u32 scan cannot overflow on closed-form leaves (|Z(x; g, h)| is not bounded by the
+            // memo-block guard)
+            uint64_t c64 = (leaf && lane < dl) ? cnt : 0ull;
+            if (lane == 0) c64 -= kfirst;
+            uint32_t c = (uint32_t)(c64 < left ? c64 : left);
             kfirst = 0;
             uint32_t incl = c;
 #pragma unroll
@@ -2161,6 +2502,18 @@ __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, Pl
     if constexpr (MODE == FZ_HASH) {
         acc_hash = warp_sum_u64(acc_hash);
         if (lane == 0) atomicAdd((unsigned long long *)(hdr->result + 1), (unsigned long long)acc_hash);
+    }
+}
+
+// ------------------------------------------------------- end-to-end ring
+// fz_run_host: fold a finished chunk's {rows, hash, err} into the run's accumulator (stream-ordered after
+// the chunk's K5, before the next chunk's K4 reuses the plan header).
+__global__ void __launch_bounds__(32) k_run_acc(const PlanHdr *h, uint64_t *acc)
+{
+    if (threadIdx.x == 0) {
+        acc[0] += h->result[0];
+        acc[1] += h->result[1];
+        acc[2] |= h->err;
     }
 }
 

@@ -52,6 +52,7 @@ def _load():
         "fz_plan_workspace_bytes": [vp, u64p],
         "fz_plan_create": [vp, u64, c_int, c_int, c_int, vp, u64, vp, ctypes.POINTER(vp)],
         "fz_plan_shard": [vp, vp, u64p, u64p, u64p],
+        "fz_plan_walk": [vp, ctypes.POINTER(c_int), ctypes.POINTER(c_int)],
         "fz_layout_create": [u32p, c_int, c_int, u64, c_int, ctypes.POINTER(vp)],
         "fz_layout_create_partial": [u32p, c_int, c_int, u64, u64, c_int, ctypes.POINTER(vp)],
         "fz_layout_workspace_bytes": [vp, u64p],
@@ -63,7 +64,7 @@ def _load():
         "fz_plan_result": [vp, vp, u64p, u64p],
         "fz_plan_result_ptr": [vp, ctypes.POINTER(vp)],
         "fz_enumerate": [vp, u64, c_int, c_int, c_int, u64, vp, u64, vp, u64, vp, u64p, u64p],
-        "fz_run_workspace_bytes": [u32p, c_int, c_int, u64, c_int, u64p],
+        "fz_run_workspace_bytes": [u32p, c_int, c_int, u64, c_int, u64, u64p],
         "fz_run_host": [u32p, c_int, c_int, u64, c_int, vp, u64, vp, u64, vp, u64p, u64p],
     }
     for name, args in sig.items():
@@ -241,6 +242,7 @@ class Plan:
     def __init__(self, memo: Memo, n: int, mode, shard: int = 0, nshards: int = 1, stream=None,
                  workspace: torch.Tensor | None = None):
         self.memo, self.n, self.mode = memo, int(n), _mode(mode)
+        self.stream = stream          # the stream K4 runs on: shard() / result() synchronise it by default
         need = plan_workspace_bytes(memo)
         if workspace is None or workspace.numel() < need:
             workspace = torch.empty(need, dtype=torch.uint8, device=memo.ws.device)
@@ -252,12 +254,21 @@ class Plan:
         self._shard = None
 
     def shard(self, stream=None):
-        """(row_begin, rows, nslices) as computed by K4 on the device (synchronises)."""
+        """(row_begin, rows, nslices) as computed by K4 on the device (synchronises the plan's stream)."""
         if self._shard is None:
             rb, rl, ns = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-            _check(_L.fz_plan_shard(self.h, _stream(stream), ctypes.byref(rb), ctypes.byref(rl), ctypes.byref(ns)))
+            s = stream if stream is not None else self.stream
+            _check(_L.fz_plan_shard(self.h, _stream(s), ctypes.byref(rb), ctypes.byref(rl), ctypes.byref(ns)))
             self._shard = (rb.value, rl.value, ns.value)
         return self._shard
+
+    WALKS = {0: "rows", 1: "deep", 2: "table", 3: "count_pairs", 4: "count_runs"}
+
+    def walk(self):
+        """(kernel kind, bytes per card lookup) of this plan's enumeration (fz_plan_walk)."""
+        k, cb = ctypes.c_int(), ctypes.c_int()
+        _check(_L.fz_plan_walk(self.h, ctypes.byref(k), ctypes.byref(cb)))
+        return self.WALKS[k.value], cb.value
 
     @property
     def row_begin(self):
@@ -285,11 +296,14 @@ class Plan:
         if out is not None:
             assert out.dtype in (torch.int32, torch.uint32) and out.is_contiguous()
             ptr, cap = out.data_ptr(), out.numel() // self.memo.d
-        _check(_L.fz_enumerate_launch(self.h, ctypes.c_void_p(ptr), cap, rb, _stream(stream)))
+        _check(_L.fz_enumerate_launch(self.h, ctypes.c_void_p(ptr), cap, rb,
+                                      _stream(stream if stream is not None else self.stream)))
 
     def result(self, stream=None):
+        """(rows, hash) of this shard after its enumeration (synchronises the plan's stream)."""
         r, h = ctypes.c_uint64(), ctypes.c_uint64()
-        _check(_L.fz_plan_result(self.h, _stream(stream), ctypes.byref(r), ctypes.byref(h)))
+        s = stream if stream is not None else self.stream
+        _check(_L.fz_plan_result(self.h, _stream(s), ctypes.byref(r), ctypes.byref(h)))
         return r.value, h.value
 
     def result_tensor(self) -> torch.Tensor:
@@ -305,7 +319,7 @@ def enumerate(memo: Memo, n: int, mode="materialize", *, out=None, shard: int = 
     """Plan + enumerate shard `shard` of Z(n).  Returns (rows tensor | None, row count, hash)."""
     plan = Plan(memo, n, mode, shard, nshards, stream=stream)
     m = plan.mode
-    if m == MATERIALIZE and out is None:
+    if m == MATERIALIZE and out is None:   # plan.rows synchronises `stream`, the one K4 ran on
         out = torch.empty((max(plan.rows, 1), memo.d), dtype=torch.int32, device=memo.ws.device)
     plan.launch(out if m == MATERIALIZE else None, row_base, stream=stream)
     rows, h = plan.result(stream=stream)
@@ -315,26 +329,29 @@ def enumerate(memo: Memo, n: int, mode="materialize", *, out=None, shard: int = 
 
 
 def run_host(gens, t: int, n: int, mode="materialize", h_out: torch.Tensor | None = None, device=None, stream=None,
-             workspace: torch.Tensor | None = None):
+             workspace: torch.Tensor | None = None, ring_bytes: int = 0):
     """Whole path from host buffers (fz_run_host).  For MATERIALIZE, h_out is a (pinned) CPU int32
-    tensor [>= |Z(n)|, d] that receives the rows.  Returns (rows, hash)."""
+    tensor [>= |Z(n)|, d] that receives the rows, streamed through a device output ring: the part of
+    `workspace` beyond the memo (allocated here with `ring_bytes` of ring, 0 = default, when None).
+    Returns (rows, hash)."""
     garr = _gens(gens)
     d, m = len(gens), _mode(mode)
-    nbytes = ctypes.c_uint64()
-    _check(_L.fz_run_workspace_bytes(garr, d, int(t), int(n), m, ctypes.byref(nbytes)))
     device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    if workspace is None or workspace.numel() < nbytes.value:
-        workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=device)
+    if workspace is None:
+        workspace = torch.empty(run_workspace_bytes(gens, t, n, mode, ring_bytes), dtype=torch.uint8, device=device)
     ptr, cap = None, 0
     if h_out is not None:
         ptr, cap = h_out.data_ptr(), h_out.numel() // d
     r, h = ctypes.c_uint64(), ctypes.c_uint64()
-    _check(_L.fz_run_host(garr, d, int(t), int(n), m, ctypes.c_void_p(workspace.data_ptr()), nbytes.value,
+    _check(_L.fz_run_host(garr, d, int(t), int(n), m, ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                           ctypes.c_void_p(ptr), cap, _stream(stream), ctypes.byref(r), ctypes.byref(h)))
     return r.value, h.value
 
 
-def run_workspace_bytes(gens, t: int, n: int, mode="materialize") -> int:
+def run_workspace_bytes(gens, t: int, n: int, mode="materialize", ring_bytes: int = 0) -> int:
+    """Device bytes fz_run_host needs: the memo, plan headers and (MATERIALIZE) an output ring of
+    `ring_bytes` (0 = the default: what the output needs, at most 64 MB)."""
     nbytes = ctypes.c_uint64()
-    _check(_L.fz_run_workspace_bytes(_gens(gens), len(gens), int(t), int(n), _mode(mode), ctypes.byref(nbytes)))
+    _check(_L.fz_run_workspace_bytes(_gens(gens), len(gens), int(t), int(n), _mode(mode), int(ring_bytes),
+                                     ctypes.byref(nbytes)))
     return nbytes.value

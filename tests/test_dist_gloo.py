@@ -18,7 +18,10 @@ import torch.multiprocessing as mp
 
 from conftest import ROOT
 
-CASES = [((11, 13, 17, 19), 4000, 2), ((13, 37, 38, 40), 5000, 2), ((6, 9, 20), 1000, 2), ((13, 37, 38, 40, 41), 1000, 3)]
+# the last case has C4's shape (d = 8, generators 97..104, t = 3): its COUNT cut is the pair walk's cost cut
+# (whole outer prefixes), the one bench.py's N > 1 headline (C4 count, one problem cut into N shards) uses
+CASES = [((11, 13, 17, 19), 4000, 2), ((13, 37, 38, 40), 5000, 2), ((6, 9, 20), 1000, 2), ((13, 37, 38, 40, 41), 1000, 3),
+         ((97, 98, 99, 100, 101, 102, 103, 104), 4500, 3)]
 
 
 def _free_port():

@@ -184,15 +184,22 @@ def test_c3_count_hash(t, corc):
 
 
 # ---------------------------------------------------------------------- C4
-def test_c4_count(corc):
-    """C4 count-only, t=3: the walk's count == the independent GF count (3 356 809 984 741)."""
-    memo = fz.memo_build(C4.gens, C4.t, C4.n + 1, entries=False)
+@pytest.mark.parametrize("t", [3, 2])
+def test_c4_count(t, corc):
+    """C4 count-only, t = 3 (u16 card image) and t = 2 (u8 image, 6.14e12 lookups): the pair walk's count ==
+    the independent GF count (3 356 809 984 741), whole and over 2 / 8 shards, in bench.py's launch
+    configuration (BASELINE configs[3])."""
+    memo = fz.memo_build(C4.gens, t, C4.n + 1, entries=False)
     want = corc.gf_count(C4.n, C4.gens)
     assert want == 3_356_809_984_741
-    assert fz.enumerate(memo, C4.n, "count")[1] == want
+    p = fz.Plan(memo, C4.n, "count")
+    assert p.walk() == ("count_pairs", 2 if t == 3 else 1)
+    p.launch()
+    assert p.result()[0] == want
     assert fz.count(memo, C4.n) == want
-    tot = sum(fz.enumerate(memo, C4.n, "count", shard=s, nshards=8)[1] for s in range(8))
-    assert tot == want
+    for k in (2, 8):
+        tot = sum(fz.enumerate(memo, C4.n, "count", shard=s, nshards=k)[1] for s in range(k))
+        assert tot == want, k
 
 
 @pytest.mark.parametrize("seed", range(32))
@@ -253,6 +260,40 @@ def test_run_host_end_to_end(corc):
         assert np.array_equal(host.numpy().view(np.uint32), want)
         assert fz.run_host(g, t, n, "hash") == (cnt, h)
         assert fz.run_host(g, t, n, "count")[0] == cnt
+
+
+# ------------------------------------------- f3: output streamed through a bounded device ring
+@pytest.mark.parametrize("ring", [1024, 4096, 1 << 20], ids=lambda r: f"ring{r}")
+def test_run_host_ring_small(ring, corc):
+    """fz_run_host streams MATERIALIZE output through a device ring
+    of 4 slots (down to 256 B = 16-21 rows a slot: thousands of chunks, every slot reused many times),
+    element by element == the oracle; the device workspace is memo + headers + ring, whatever |Z(n)|."""
+    for g, n, t in (((13, 37, 38, 40), 5000, 2), ((6, 9, 20), 1000, 2), ((13, 37, 38, 40, 41), 1500, 3),
+                    ((23, 29, 31), 3001, 1)):
+        want, cnt, h = corc.enumerate(n, g, use_o2=True)
+        nb = fz.run_workspace_bytes(g, t, n, "materialize", ring_bytes=ring)
+        lay = fz.Layout(g, t, n + 1, memo_top=fz.MEMO_TOP_AUTO)
+        assert nb <= lay.workspace_bytes + 4096 + max(ring, 4 * 256)     # bounded: not |Z(n)| * 4 d
+        ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        host = torch.empty((max(cnt, 1), len(g)), dtype=torch.int32).pin_memory()
+        r, hh = fz.run_host(g, t, n, "materialize", host, workspace=ws)
+        assert r == cnt
+        assert np.array_equal(host.numpy().view(np.uint32)[:cnt], want.reshape(-1, len(g))), (g, n, ring)
+
+
+def test_run_host_ring_c2(corc):
+    """C2's 1.6 GB output streams through a 64 MB device ring (workspace < 128 MB) into pinned host memory,
+    element by element == O2 (BASELINE configs[1])."""
+    g, n, t = C2.gens, C2.n, C2.t
+    nb = fz.run_workspace_bytes(g, t, n, "materialize", ring_bytes=64 << 20)
+    assert nb < (128 << 20)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    want, cnt, h = corc.enumerate(n, g, use_o2=True)
+    host = torch.empty((cnt, len(g)), dtype=torch.int32).pin_memory()
+    r, _ = fz.run_host(g, t, n, "materialize", host, workspace=ws)
+    assert r == cnt == 100_000_681
+    assert np.array_equal(host.numpy().view(np.uint32), want.reshape(-1, len(g)))
+    assert fz.run_host(g, t, n, "hash", workspace=ws) == (cnt, h)
 
 
 # ------------------------------------------------------- f1: full DP table (t = d)

@@ -33,7 +33,12 @@ def shard_times(g, n, t, mode, k, reps=3):
 
 
 fz.set_memo_cap(64 << 30)
-for name, g, n, t, mode in (("C4 count t=3", C4.gens, C4.n, 3, "count"), ("C3 hash t=3", C3_GENS, C3_N, 3, "hash")):
+CASES = (("C4 count t=3", C4.gens, C4.n, 3, "count"), ("C4 count t=2", C4.gens, C4.n, 2, "count"),
+         ("C3 hash t=3", C3_GENS, C3_N, 3, "hash"))
+want = sys.argv[1:]   # e.g. C4 -> both C4 rows
+for name, g, n, t, mode in CASES:
+    if want and not any(name.startswith(w) for w in want):
+        continue
     t1 = shard_times(g, n, t, mode, 1)[0]
     print(f"{name}: 1 shard {t1:.3f} ms")
     for k in (2, 4, 8):
