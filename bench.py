@@ -517,6 +517,83 @@ def run_reference(args, rank, world):
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+# ------------------------------------------------------------------ f4 study (not part of the default run)
+def cpu_baseline_memo(g, t: int, top: int, reps: int = 3) -> float:
+    """The paper's CPU memo variant (Alg. LexicographicFactorizationListsUpToElement, PAPER.md:139-153,
+    single thread; Table 1's cpu_memo_us column) as the oracle implements it (orc_memo_alg2),
+    timed on this host: the CPU side of the f4 CPU-vs-GPU memo crossover.  Microseconds,
+    median of `reps`."""
+    from oracle import oracle as O
+
+    C, tail = O.C(), tuple(g[len(g) - t:])
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        C.memo_alg2(tail, top)
+        ts.append((time.perf_counter() - t0) * 1e6)
+    return sorted(ts)[len(ts) // 2]
+
+
+def f4_study(args):
+    """SURVEY §8(f) f4 (PAPER.md:194 both memo variants timed; PAPER.md:301 the best memoDim depends on the
+    instance): for Table 1's 31 rows (materialize), C2 (materialize), C3 (hash) and C4 (count), the whole-step
+    time (memo build + plan + K5, CUDA events, median of 5) for every memo dimension t the cost model does not
+    rule out by 30x, the GPU memo build alone and, for Table 1 rows, the single-thread CPU memo (oracle Alg 2)
+    at the paper's t.  One JSON object per line; tools/f4_fit.py fits fz_recommend_t's constants to it."""
+    import torch
+
+    from fzinputs import C2, C3_GENS, C3_N, C4, TABLE1_ROWS, table1_gens
+    from paper_2407_20474_b200 import fz
+
+    fz.set_memo_cap(64 << 30)
+
+    def timed(fn, reps=5, warm=2):
+        for _ in range(warm):
+            fn()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        return sorted(ts)[len(ts) // 2]
+
+    cases = [(f"T1 d={d} n={n}", table1_gens(d), n, "materialize", md) for d, md, n in TABLE1_ROWS]
+    cases += [("C2", C2.gens, C2.n, "materialize", C2.t), ("C3", C3_GENS, C3_N, "hash", 3), ("C4", C4.gens, C4.n,
+                                                                                              "count", C4.t)]
+    for name, g, n, mode, tp in cases:
+        d = len(g)
+        _, pred = fz.recommend_t(g, n, mode)
+        best_pred = min(pred.values()) if pred else None
+        rec = {"case": name, "gens": list(g), "n": n, "mode": mode, "t_paper": tp, "pred_s": pred, "step_us": {},
+               "memo_us": {}}
+        for t in range(1, d):
+            if t not in pred or pred[t] > 30 * best_pred:
+                continue
+            try:
+                lay = fz.Layout(g, t, n + 1, entries=mode != "count")
+            except fz.FzError:
+                continue
+            ws = torch.empty(lay.workspace_bytes, dtype=torch.uint8, device="cuda")
+            memo = fz.Memo(layout=lay, workspace=ws)
+            pws = torch.empty(fz.plan_workspace_bytes(memo), dtype=torch.uint8, device="cuda")
+            rows = fz.Plan(memo, n, mode, workspace=pws).rows
+            out = torch.empty((max(rows, 1), d), dtype=torch.int32, device="cuda") if mode == "materialize" else None
+
+            def step():
+                m = fz.Memo(layout=lay, workspace=ws)
+                fz.Plan(m, n, mode, workspace=pws).launch(out)
+            reps = 3 if pred[t] > 0.05 else 5
+            rec["step_us"][t] = timed(step, reps=reps, warm=1 if pred[t] > 0.05 else 2)
+            rec["memo_us"][t] = timed(lambda: fz.Memo(layout=lay, workspace=ws), reps=5)
+            del out, ws
+        if name.startswith("T1"):
+            rec["cpu_memo_us"] = cpu_baseline_memo(g, tp, n + 1)
+        print(json.dumps(rec), flush=True)
+
+
 def _free_port() -> int:
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -544,12 +621,16 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-count", action="store_true", help="skip the extra legs")
     ap.add_argument("--no-hash", action="store_true")
+    ap.add_argument("--study", default=None, choices=["f4"], help="run a study instead of the bench line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local_rank = _env_int("LOCAL_RANK", 0)
 
+    if args.study == "f4":
+        f4_study(args)
+        return
     if args.impl == "reference":
         res = run_reference(args, rank, world)
         if res is not None:

@@ -174,8 +174,9 @@ struct Sizing {
     Layout lay{};
 };
 
-constexpr uint64_t kCountRunCost = 32;     // COUNT pair-walk cost model (card lookups): per innermost run
-constexpr uint64_t kCountOuterCost = 0;    // ... and per outer prefix
+constexpr uint64_t kCountRunCost = 64;     // COUNT pair-walk cost model (card lookups; measured, tools/count_tune.py): per innermost run
+constexpr uint64_t kCountOuterCost = 1024;  // ... and per outer prefix
+constexpr uint64_t kWordStreamRowsPerPrefix = 36;   // MATERIALIZE word stream from this many rows per prefix
 constexpr uint64_t kSmemMax = 220 * 1024;   // dynamic shared memory budget of the ring fill
 constexpr int kMaxGrid = 1024;              // chunk scratch entries of the K1 grid
 
@@ -336,6 +337,8 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
         if (forced >= 1 && forced <= 5 && !(forced == 1 && !fit) && !(forced == 4 && !chains_fit) &&
             (ltop == top || forced == 5))
             z.fill_mode = forced;
+        else if (t >= 5 && chains_fit && ltop == top)
+            z.fill_mode = 4;   // deep tails: chains stepped in order beat the scan form (measured, tools/fill_modes.py)
         else
             z.fill_mode = 5;
     } else {
@@ -509,7 +512,10 @@ PairPlan pair_plan(const fz_layout *lay, uint64_t n)
     g.R16 = (uint32_t)R16;
     g.ncolv = e * (mp + dup);
     // flush period (iterations of 4 cards per packed lane: a Y and an X word pair)
+    // flush period of the packed accumulators (iterations; each adds 4 cards per packed lane: two Y words, two
+    // X words), a multiple of 4 (the unrolled step) when at least 4
     g.F = cmax == 0 ? (1u << 30) : (uint32_t)((u8 ? 255ull : 65535ull) / (4 * cmax));
+    if (g.F >= 4) g.F &= ~3u;
     auto m32 = [](uint64_t v) -> uint32_t { return v == 1 ? 0xffffffffu : (uint32_t)((1ull << 32) / v); };
     g.Mm = m32(m);
     g.Mg2 = m32(g2);
@@ -704,12 +710,17 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     const size_t smem = (size_t)(f0n + 1) / 2 * 16 + (c16R ? cbytes : 0);
     // persistent grid: exactly the resident CTAs (the walk is a grid-stride loop over slices)
     int per_sm = 0;
-    // (static shared memory -- the MATERIALIZE word-stream staging -- plus this dynamic part may pass 48 KB)
-    FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // grid sized for the largest dynamic part any n can ask (the 32 KB level-0 cache), so the residency does
+    // not depend on n; the attribute must allow that size for the occupancy query (static shared memory --
+    // the MATERIALIZE word-stream staging -- plus the dynamic part may pass 48 KB)
+    const size_t smem_q = std::max<size_t>(smem, 4096 * 8);
+    FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::walk_threads<MODE>(),
-                                                      std::max<size_t>(smem, 4096 * 8)) != cudaSuccess ||
-        per_sm < 1)
+                                                      smem_q) != cudaSuccess ||
+        per_sm < 1) {
+        cudaGetLastError();
         per_sm = 1;
+    }
     per_sm = std::min(per_sm, 8);
     FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE>, dim3((unsigned)(device_sms() * per_sm)),
                        dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
@@ -1368,6 +1379,13 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
         a.wt.gmag[j] = (g == 1) ? 0 : (~0ull / g + 1);   // ceil(2^64 / g)
     }
     a.wt.card64 = m->S + (uint64_t)z.L * z.top;
+    {   // d not a multiple of 4: rows leave as a 16-B word stream when the warp rounds are long (measured on
+        // Table 1 rows: it pays from ~36 rows per leading prefix); FZ_WORD_STREAM=0/1 forces
+        const char *e = getenv("FZ_WORD_STREAM");
+        const uint64_t P = m->lay->H.W.empty() ? 0 : m->lay->H.W[p->n];
+        const bool long_rounds = P && m->lay->H.S[p->n] >= kWordStreamRowsPerPrefix * P;
+        a.wt.word_stream = (e && *e) ? (e[0] != '0') : long_rounds;
+    }
     a.card_max = z.card_max_all;
     a.prefixes = m->lay->H.W.empty() ? 0 : m->lay->H.W[p->n];
     a.out = d_out;

@@ -1510,6 +1510,7 @@ struct WalkTables {
     uint64_t gmag[kMaxD];    // division magic of each generator: x / g_j = umulhi64(x, gmag[j]) (+x if g_j = 1)
     uint32_t m;              // g_L (residue modulus of cardT / offT)
     uint64_t R;              // rows per residue column
+    int word_stream;         // MATERIALIZE, d not a multiple of 4: write rows as a 16-B word stream
 };
 
 
@@ -1537,7 +1538,8 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     __shared__ BlockInfo binfo[MODE == FZ_COUNT ? 1 : kWalkThreads / 32][32];   // MAT/HASH block lists
     // MATERIALIZE with d not a multiple of 4: per-warp staging of 128 rows as a word stream (+ 3 words of phase)
     constexpr bool kWordStream = MODE == FZ_MATERIALIZE && (D % 4) != 0;
-    __shared__ __align__(16) uint32_t wsb[kWordStream ? kWalkThreads / 32 : 1][kWordStream ? 128 * D + 4 : 1];
+    constexpr int kUnr = (MODE == FZ_MATERIALIZE) ? 4 : 2;   // 32-row chunks per store group (d >= 7 with 2: slower)
+    __shared__ __align__(16) uint32_t wsb[kWordStream ? kWalkThreads / 32 : 1][kWordStream ? 32 * kUnr * D + 4 : 1];
     const int lane = threadIdx.x & 31, wib = (MODE == FZ_COUNT) ? 0 : threadIdx.x >> 5;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -1762,7 +1764,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 // flattened copy: rows q0 + lane of the round, owner block via block-start bitmask.
                 // UNR chunks of 32 rows are resolved and their memo tails loaded before any store,
                 // so each lane keeps UNR L2 loads in flight.
-                constexpr int UNR = (MODE == FZ_MATERIALIZE) ? 4 : 2;
+                constexpr int UNR = kUnr;
                 const uint32_t rel = cc > 0 ? excl : 0xffffffffu;   // this lane's block start (none: ~0)
                 uint32_t lm_le;                                       // lanes 0..lane
                 asm("mov.u32 %0, %%lanemask_le;" : "=r"(lm_le));
@@ -1794,7 +1796,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                             }
                         }
                     }
-                    if constexpr (kWordStream) {
+                    if (kWordStream && wt.word_stream) {
                         // d not a multiple of 4: the warp's rows [q0, q0 + nr) are one contiguous run of nr d
                         // words; stage them in shared memory at the 16-B phase of their global address and
                         // write the aligned middle as 16-B vectors (scalar head and tail words)
@@ -1896,7 +1898,8 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
 // lane reads vector j of Y and of X (while X has one) in the same iteration -- the same vector index in
 // every lane, which keeps the loads conflict-free -- adding the packed u16 (u8) words with IADD3 into two
 // packed accumulators that dp2a (dp4a) unpacks every F iterations (F = 65535 / (4 card_max), resp.
-// 255 / (4 card_max)); the masked last vector of each run is read once, its mask computed in registers.
+// 255 / (4 card_max), a multiple of 4); the last, partial vector of each run is read once and summed by
+// dp2a / dp4a with 0/1 byte selectors for its first entries (no masking of the data).
 //
 // Slices: cost ranks of the C tables (C_{L-2}[R] = W_{L-2}[R] + beta (A + 1) + gamma: a run costs its
 // lookups plus beta, an outer prefix gamma more), guided sizes (gss_begin).  A slice [b, e) takes the
@@ -2090,12 +2093,7 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
         // slice.  The common step (only a_{L-3} decrements, R += g3) updates R, A, rmin, col, idx0 without
         // division.
         auto advance = [&]() -> bool {
-            int i = -1;
-#pragma unroll
-            for (int j = 0; j < NO; ++j)
-                if (o[j] > 0) i = j;
-            if (i < 0) return false;
-            if (i == NO - 1) {
+            if (o[NO - 1] > 0) {   // the common step: only a_{L-3} decrements
                 o[NO - 1] -= 1;
                 rj[NO] += G.g[NO - 1];
                 if (at_end()) return false;
@@ -2118,6 +2116,11 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
                 c = 0;
                 return true;
             }
+            int i = -1;
+#pragma unroll
+            for (int j = 0; j < NO - 1; ++j)
+                if (o[j] > 0) i = j;
+            if (i < 0) return false;
 #pragma unroll
             for (int j = 0; j < NO; ++j) {
                 if (j == i) o[j] -= 1;
@@ -2138,14 +2141,21 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
             while (filled < 32 && live) {
                 const uint32_t P = A / 2 + 1;
                 const uint32_t take = (P - c < 32 - filled) ? P - c : 32 - filled;
+                // orbit positions of the group's first X run and (minus 31) its first Y run, mod m' (uniform);
+                // without duplicate columns the lanes reduce their own positions
+                uint32_t bx = idx0 + c, by = idx0 + A + 32 * pg.mp - c - 31;
+                if (pg.dup) {
+                    bx -= div32(bx, pg.mp, pg.Mmp) * pg.mp;
+                    by -= div32(by, pg.mp, pg.Mmp) * pg.mp;
+                }
                 if ((uint32_t)lane >= filled && (uint32_t)lane < filled + take) {
                     mine = true;
                     mR = R;
                     mA = A;
                     mrmin = rmin;
                     mcb = cb;
-                    mbx = idx0 + c;
-                    mby = idx0 + A + 32 * pg.mp - c - 31;
+                    mbx = bx;
+                    mby = by;
                     mpp = c;
                     mf = filled;
                 }
@@ -2160,8 +2170,8 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
                 lenX = (2 * pp == mA) ? 0u : div32(mrmin + pp * g2, m, pg.Mm) + 1;
                 lenY = div32(mR - pp * g2, m, pg.Mm) + 1;
                 if (pg.dup) {   // 32 consecutive stored columns per group, ascending / descending
-                    jX = mbx - div32(mbx, pg.mp, pg.Mmp) * pg.mp + li;
-                    jY = mby - div32(mby, pg.mp, pg.Mmp) * pg.mp + 31 - li;
+                    jX = mbx + li;
+                    jY = mby + 31 - li;
                 } else {
                     const uint32_t x = mbx + li, y = mby + 31 - li;
                     jX = x - div32(x, pg.mp, pg.Mmp) * pg.mp;
@@ -2173,9 +2183,9 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
             // vector j of Y and of X (while X has one) in the same iteration: every lane reads vector index j
             // of its columns, so the 8 lanes of a quarter-warp stay in distinct bank groups
             uint32_t sum = 0, j = 0;
-            while (j < NY) {
+            while (j < NY) {   // chunks of F iterations (F a multiple of 4: the 1-step loop runs in the last only)
                 const uint32_t je = (NY - j < pg.F) ? NY : j + pg.F;
-                uint32_t a0 = 0, a1 = 0;
+                uint32_t a0 = 0, a1 = 0;   // packed: words 0-1, 2-3 of Y and X vectors
 #pragma unroll 1
                 for (; j + 4 <= je; j += 4) {
                     const uint4 y0 = lds128(ya), y1 = lds128(ya + 16), y2 = lds128(ya + 32), y3 = lds128(ya + 48);

@@ -9,6 +9,7 @@ chosen so that a plausible slip (dropped term, wrong index, reversed order,
 transposed operand) fails at least one test.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -264,6 +265,18 @@ def test_hash_kats(kat, corc):
 def test_hash_kats_mid(kat, corc):
     g, n = parse_gens(kat["gens"]), int(kat["n"])
     assert corc.count_hash(n, g, use_o2=True) == (int(kat["count"]), int(kat["H"], 16))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kat", [k for k in HASH_KATS if k["tier"] == "big"],
+                         ids=lambda k: f"{k['gens']}-{k['n']}")
+def test_hash_kats_big(kat, corc):
+    """The big-tier KATs (C3: Z(17350; 23..43), 1.0e10 rows; the C4 shape Z(10000; 97..104), 2.5e8 rows)
+    reproduced by oracle/ itself (O2 + R17, OpenMP over a_1): closes the chain from SURVEY App. A's scratch
+    values to the constants the GPU tests assert (test_c3_count_hash, test_c4_shape_hash).  ~1-2 min on 8 cores."""
+    g, n = parse_gens(kat["gens"]), int(kat["n"])
+    assert corc.count_hash(n, g, use_o2=True, threads=len(os.sched_getaffinity(0))) == \
+        (int(kat["count"]), int(kat["H"], 16))
 
 
 def test_hash_properties():

@@ -19,6 +19,11 @@ CFG = {
     "C4t4": ((97, 98, 99, 100, 101, 102, 103, 104), 40000, 4, "count"),
     "C4": ((97, 98, 99, 100, 101, 102, 103, 104), 40000, 3, "count"),
     "T1": ((13, 37, 38, 40, 41, 42, 43, 44), 2000, 4, "materialize"),
+    "T95": ((13, 37, 38, 40, 41, 42, 43, 44, 45), 1500, 5, "materialize"),
+    "T94": ((13, 37, 38, 40, 41, 42, 43, 44, 45), 1500, 4, "materialize"),
+    "T63": ((13, 37, 38, 40, 41, 42), 5000, 3, "materialize"),
+    "T31": ((13, 37, 38), 300000, 1, "materialize"),
+    "T74": ((13, 37, 38, 40, 41, 42, 43), 2000, 4, "materialize"),
 }
 # partial memo (f2): memo rows only for x < frac * n
 for _f in (10, 25, 50, 75, 90):
