@@ -149,7 +149,7 @@ fz_status host_tables(const uint32_t *g, int d, int L, uint64_t top, HostTables 
 }
 
 struct Layout {
-    uint64_t S, W, C, cardT, off, offT, chunk, links, rows, counter, list, total;
+    uint64_t S, W, C, cardT, off, offT, chunk, links, rows, rows16, counter, list, total;
 };
 
 struct Sizing {
@@ -177,6 +177,8 @@ struct Sizing {
 constexpr uint64_t kCountRunCost = 64;     // COUNT pair-walk cost model (card lookups; measured, tools/count_tune.py): per innermost run
 constexpr uint64_t kCountOuterCost = 1024;  // ... and per outer prefix
 constexpr uint64_t kWordStreamRowsPerPrefix = 36;   // MATERIALIZE word stream from this many rows per prefix
+constexpr uint64_t kRows16MinBytes = 64ull << 20;   // u16 row copy: u32 rows above this (half the 126 MB L2)
+constexpr uint64_t kRows16MaxBytes = 96ull << 20;   //   ... and the copy below this
 constexpr uint64_t kSmemMax = 220 * 1024;   // dynamic shared memory budget of the ring fill
 constexpr int kMaxGrid = 1024;              // chunk scratch entries of the K1 grid
 
@@ -229,7 +231,10 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
         if (__builtin_add_overflow(entries, card[x], &entries)) return fail(FZ_ERANGE, "memo entries exceed 2^64");
         mx = std::max(mx, card[x]);
     }
-    if (mx >= (1ull << 26)) return fail(FZ_ERANGE, "a memo block has %llu >= 2^26 rows", (unsigned long long)mx);
+    // memo blocks are copied and indexed with 32-bit row counts per warp round (< 2^26); a count-only layout
+    // holds no blocks (its COUNT walk reads the u32 card table: fz_plan_create checks < 2^32)
+    if (with_entries && t > 0 && mx >= (1ull << 26))
+        return fail(FZ_ERANGE, "a memo block has %llu >= 2^26 rows", (unsigned long long)mx);
     z.entries = entries;
     z.max_card = mx;
     uint32_t b = 0xffffffffu, hmax = 0;
@@ -359,6 +364,17 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
     if (z.fill_mode == 1) p = align_up(p + 4ull * entries + 64, 256);
     if (z.fill_mode == 2) p = align_up(p + 8ull * entries, 256);
     l.rows = p;    p = align_up(p + rows_bytes + 64, 256);
+    // u16 copy of the rows for the walks (k3_pack16) when the u32 rows overflow L2 but the u16 copy does not
+    // and every coordinate is below 2^16 (C3 t = 3: 162 MB -> 81 MB)
+    l.rows16 = 0;
+    if (z.fill_mode && rows_bytes > kRows16MinBytes && entries * 2ull * t <= kRows16MaxBytes) {
+        uint32_t gmin = 0xffffffffu;
+        for (int i = L; i < d; ++i) gmin = std::min(gmin, g[i]);
+        if ((ltop - 1) / gmin < 65536) {
+            l.rows16 = p;
+            p = align_up(p + entries * 2ull * t + 64, 256);
+        }
+    }
     l.list = p;    if (z.fill_mode == 5) p = align_up(p + z.list_bytes, 256);
     l.total = p;
     return FZ_OK;
@@ -381,6 +397,7 @@ struct fz_memo {
     char *ws;
     uint64_t *S, *W, *C, *off, *offT, *chunk;
     uint32_t *cardT, *rows;
+    uint16_t *rows16;      // u16 copy of the rows, or nullptr
     void *links;
     unsigned int *counter;
 };
@@ -722,9 +739,20 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
         per_sm = 1;
     }
     per_sm = std::min(per_sm, 8);
-    FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE>, dim3((unsigned)(device_sms() * per_sm)),
-                       dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
-                       a.wt, a.out, (uint64_t)a.cap, (uint64_t)a.row_base, f0n, c16R));
+    bool m16 = false;
+    if constexpr (MODE == FZ_HASH) m16 = a.wt.memo16 != nullptr;
+    if constexpr (MODE == FZ_HASH) if (m16) {   // the u16 copy of the rows (same grid: same registers and smem)
+        FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_q));
+        FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE, true>, dim3((unsigned)(device_sms() * per_sm)),
+                           dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
+                           a.wt, a.out, (uint64_t)a.cap, (uint64_t)a.row_base, f0n, c16R));
+    }
+    if (!m16) {
+        FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE>, dim3((unsigned)(device_sms() * per_sm)),
+                           dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
+                           a.wt, a.out, (uint64_t)a.cap, (uint64_t)a.row_base, f0n, c16R));
+    }
     ++g_launches;
     return cuda_check("k5_walk");
 }
@@ -1067,6 +1095,7 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
     m->counter = (unsigned int *)(w + z.lay.counter);
     m->links = (void *)(w + z.lay.links);
     m->rows = (uint32_t *)(w + z.lay.rows);
+    m->rows16 = z.lay.rows16 ? (uint16_t *)(w + z.lay.rows16) : nullptr;
     cudaStream_t s = (cudaStream_t)stream;
     Gens G = make_gens(lay->g, z.d);
     fzk::Tables tb;
@@ -1121,6 +1150,13 @@ fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_byt
         return cuda_check("k1_tables");
     }();
     if (!st && !(z.fill_mode == 5 && g_fuse_memo)) st = launch_fill(m, s);
+    if (!st && m->rows16) {   // the u16 copy of the rows for the walks
+        const uint64_t words = z.entries * (uint64_t)z.t;
+        fzk::k3_pack16<<<(unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)device_sms() * 16), 256, 0, s>>>(
+            m->rows, m->rows16, words);
+        ++g_launches;
+        st = cuda_check("k3_pack16");
+    }
     if (st) {
         delete m;
         return st;
@@ -1180,54 +1216,70 @@ fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards,
     return host_shards(m->lay, n, mode, nshards, row_begin, rows);
 }
 
-// SURVEY §8(f) f4 (the best memo dimension depends on the instance).  Predicted
-// seconds for memo dimension t, from the host count tables:
-//   rows R = |Z(n)|, leading prefixes P(t), innermost runs Q(t) (leading prefixes without the last
-//   coordinate), memo rows E(t) = sum_{x<=n} |Z(x; tail_t)|;
-//   MATERIALIZE: R 4d / 6.5e12 + 8e-12 P + E 4t / 2e12 + 6e-5
-//   HASH:        4e-12 R + 7.4e-12 P + E 4t / 2e12 + 6e-5
-//   COUNT:       6.2e-11 Q + 1e-13 P + 6e-5        (no memo rows are built)
-// constants: B200 measurements of round 1 (C2, C3 t=2/3, C4 t=3).  Memos above the
-// memory cap are infeasible (cost +inf).
+// SURVEY §8(f) f4 (the best memo dimension depends on the instance).  Predicted seconds
+// of a whole step (memo build + plan + walk) for memo dimension t, from the host count tables:
+//   R = |Z(n)|, P = leading prefixes (a_1..a_L, phi <= n), E = memo rows sum_{x<=n} |Z(x; tail)|, L = d - t;
+//   MATERIALIZE: 1.03e-4 + 2.815e-13 (4 d R) + 8.886e-12 P + 9.803e-13 (4 t E)
+//   HASH:        3.449e-12 R + 7.08e-12 P + 5.271e-13 (4 t E)
+//   COUNT:       8.74e-5 + c_P P, c_P = 9.4e-14 with the staged pair walk (L >= 3, cards < 2^14, image fits
+//                shared memory), else 9.2e-13 (the u32 card table from L2)
+// The constants are a non-negative least-squares fit (relative error) of B200 step times over every t of
+// Table 1's 31 rows, C2, C3 and C4 (tools/f4_fit.py on profiles/r02_f4_study.jsonl, from
+// `bench.py --study f4`).  Memos above the memory cap, and COUNT with a tail block >= 2^32, are infeasible.
 fz_status fz_recommend_t(const uint32_t *gens, int d, uint64_t n, fz_mode mode, int *t_best, double *cost)
 {
     if (!t_best) return fail(FZ_EINVAL, "t_best is NULL");
     fz_status st = validate(gens, d, d > 1 ? 1 : 0, n + 1);
     if (st) return st;
     const uint64_t top = n + 1;
-    HostTables H;
-    if ((st = host_tables(gens, d, 0, top, H))) return st;   // S levels (suffix counts) only
     double best = 1e300;
     int bt = d > 1 ? 1 : 0;
-    for (int t = 0; t <= d; ++t) {
-        double c = 1e300;
-        const int L = d - t;
-        if (t >= 1 && t <= d - 1) {
-            // P(t): prefixes (a_1..a_L) with phi <= n = sum_{y<=n} |Z(y; g_1..g_L)|; Q(t) with L-1 gens
-            auto cum = [&](int nl) -> double {
-                std::vector<double> c2(top, 0.0);
-                c2[0] = 1;
-                for (int i = 0; i < nl; ++i)
-                    for (uint64_t x = gens[i]; x < top; ++x) c2[x] += c2[x - gens[i]];
-                double sum = 0;
-                for (uint64_t x = 0; x < top; ++x) sum += c2[x];
-                return sum;
-            };
-            const double P = cum(L), Q = cum(L - 1);
-            const double R = (double)H.S[n];
-            double E = 0;
-            const uint64_t *card = H.S.data() + (size_t)L * top;
-            for (uint64_t x = 0; x < top; ++x) E += (double)card[x];
-            const bool fits = E * 4.0 * t <= (double)g_memo_cap;
-            if (mode == FZ_MATERIALIZE && fits) c = R * 4.0 * d / 6.5e12 + 8e-12 * P + E * 4.0 * t / 2e12 + 6e-5;
-            if (mode == FZ_HASH && fits) c = 4e-12 * R + 7.4e-12 * P + E * 4.0 * t / 2e12 + 6e-5;
-            if (mode == FZ_COUNT) c = 6.2e-11 * Q + 1e-13 * P + 6e-5;
+    try {
+        HostTables H;
+        if ((st = host_tables(gens, d, 0, top, H))) return st;   // S levels (suffix counts) only
+        // cumulative prefix counts over the first nl generators: sum_{y<=n} |Z(y; g_1..g_nl)|
+        auto cum = [&](int nl) -> double {
+            std::vector<double> c2(top, 0.0);
+            c2[0] = 1;
+            for (int i = 0; i < nl; ++i)
+                for (uint64_t x = gens[i]; x < top; ++x) c2[x] += c2[x - gens[i]];
+            double sum = 0;
+            for (uint64_t x = 0; x < top; ++x) sum += c2[x];
+            return sum;
+        };
+        const double R = (double)H.S[n];
+        const uint64_t cap = g_memo_cap.load();
+        for (int t = 0; t <= d; ++t) {
+            double c = 1e300;
+            const int L = d - t;
+            if (t >= 1 && t <= d - 1) {
+                const double P = cum(L);
+                double E = 0;
+                uint64_t cmax = 0;
+                const uint64_t *card = H.S.data() + (size_t)L * top;
+                for (uint64_t x = 0; x < top; ++x) {
+                    E += (double)card[x];
+                    cmax = std::max(cmax, card[x]);
+                }
+                const bool fits = E * 4.0 * t <= (double)cap;
+                if (mode == FZ_MATERIALIZE && fits)
+                    c = 1.03e-4 + 2.815e-13 * (4.0 * d * R) + 8.886e-12 * P + 9.803e-13 * (4.0 * t * E);
+                if (mode == FZ_HASH && fits) c = 3.449e-12 * R + 7.08e-12 * P + 5.271e-13 * (4.0 * t * E);
+                if (mode == FZ_COUNT && cmax < (1ull << 32)) {
+                    const uint64_t m = gens[L - 1];
+                    const double img = double(n + 1 + 32 * (n / m + 1)) * (cmax <= 63 ? 1.0 : 2.0);
+                    const bool pairs = L >= 3 && cmax <= 16383 && img <= (double)kPairSmemMax;
+                    c = 8.74e-5 + (pairs ? 9.4e-14 : 9.2e-13) * P;
+                }
+            }
+            if (cost) cost[t] = c;
+            if (c < best) {
+                best = c;
+                bt = t;
+            }
         }
-        if (cost) cost[t] = c;
-        if (c < best) {
-            best = c;
-            bt = t;
-        }
+    } catch (const std::bad_alloc &) {
+        return fail(FZ_ECAP, "host tables for n=%llu do not fit host memory", (unsigned long long)n);
     }
     *t_best = bt;
     return FZ_OK;
@@ -1371,6 +1423,7 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
     a.wt.cardT = m->cardT;
     a.wt.offT = m->offT;
     a.wt.memo = m->rows;
+    a.wt.memo16 = (p->mode == FZ_HASH) ? m->rows16 : nullptr;   // MATERIALIZE is bound by its stores
     const uint64_t gl = z.L > 0 ? m->lay->g[z.L - 1] : 1;
     a.wt.R = (z.top + gl - 1) / gl;
     a.wt.m = (uint32_t)gl;

@@ -1461,6 +1461,21 @@ __device__ __forceinline__ void load_tail(const uint32_t *__restrict__ p, uint32
     }
 }
 
+template <int T>
+__device__ __forceinline__ void load_tail16(const uint16_t *__restrict__ p, uint32_t *w)
+{
+#pragma unroll
+    for (int j = 0; j < T; ++j) asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(w[j]) : "l"(p + j));
+}
+
+// u16 copy of the memo rows (flat: every coordinate narrowed; the host checked they are < 2^16)
+__global__ void __launch_bounds__(256) k3_pack16(const uint32_t *__restrict__ rows, uint16_t *__restrict__ out,
+                                                  uint64_t words)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (uint16_t)__ldg(rows + i);
+}
+
 template <int D>
 __device__ __forceinline__ void store_row(uint32_t *p, const uint32_t (&w)[D])
 {
@@ -1506,6 +1521,7 @@ struct WalkTables {
     const uint32_t *cardT;   // residue-major card (w.r.t. m = g_L)
     const uint64_t *offT;    // residue-major CSR offsets
     const uint32_t *memo;    // CSR rows, t u32 each
+    const uint16_t *memo16;  // the same rows as t u16 each (large memos with small coordinates), or nullptr
     const uint64_t *card64;  // card = S_L, natural layout
     uint64_t gmag[kMaxD];    // division magic of each generator: x / g_j = umulhi64(x, gmag[j]) (+x if g_j = 1)
     uint32_t m;              // g_L (residue modulus of cardT / offT)
@@ -1514,7 +1530,7 @@ struct WalkTables {
 };
 
 
-template <int D, int T, int MODE>
+template <int D, int T, int MODE, bool M16 = false>
 __global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : 2)))
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
@@ -1756,7 +1772,8 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 if (cc > 0) {
                     const int e = __popc(nz & ((1u << lane) - 1));
                     // byte address of the block's memo rows, pre-offset by its first output row (u64 wrap)
-                    bi[e].memo_row = (uint64_t)(uintptr_t)wt.memo + (mrow - excl) * (uint64_t)(4 * (T > 0 ? T : 1));
+                    bi[e].memo_row = M16 ? (uint64_t)(uintptr_t)wt.memo16 + (mrow - excl) * (uint64_t)(2 * (T > 0 ? T : 1))
+                                         : (uint64_t)(uintptr_t)wt.memo + (mrow - excl) * (uint64_t)(4 * (T > 0 ? T : 1));
                     bi[e].start = excl;
                     bi[e].v = (uint32_t)vv;
                 }
@@ -1789,8 +1806,12 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                             wv[u][L - 1] = info.v;
                             if constexpr (T > 0) {
                                 uint32_t tw[T];
-                                load_tail<T>(reinterpret_cast<const uint32_t *>(info.memo_row + (uint64_t)q * (4 * T)),
-                                             tw);
+                                if constexpr (M16)   // u16 copy: half the L2 / DRAM bytes per row
+                                    load_tail16<T>(reinterpret_cast<const uint16_t *>(info.memo_row + (uint64_t)q * (2 * T)),
+                                                   tw);
+                                else
+                                    load_tail<T>(reinterpret_cast<const uint32_t *>(info.memo_row + (uint64_t)q * (4 * T)),
+                                                 tw);
 #pragma unroll
                                 for (int j = 0; j < T; ++j) wv[u][L + j] = tw[j];
                             }

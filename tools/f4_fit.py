@@ -2,14 +2,15 @@
 
     python tools/f4_fit.py profiles/r02_f4_study.jsonl
 
-Per (case, t) features from the host count tables (the same quantities fz_recommend_t computes): R = |Z(n)|,
+Per (case, t) features from the host count tables (the quantities fz_recommend_t computes): R = |Z(n)|,
 P = leading prefixes (a_1..a_L, phi <= n), Q = innermost runs (a_1..a_{L-1}), O = outer prefixes
-(a_1..a_{L-2}), E = memo rows sum_{x<=n} |Z(x; tail)|, L = d - t.  Model per mode (seconds):
+(a_1..a_{L-2}), E = memo rows sum_{x<=n} |Z(x; tail)|, L = d - t.  Whole-step model (non-negative least
+squares on relative error; seconds) -- the form fz_recommend_t evaluates:
   MATERIALIZE: c0 + c1 (4 d R) + c2 P + c3 (4 t E)
   HASH:        c0 + c1 R + c2 P + c3 (4 t E)
-  COUNT:       c0 + c1 P + c2 Q + c3 O
-fitted by non-negative least squares on relative error; prints the constants and, per case, the model's pick
-against the measured best t."""
+  COUNT:       c0 + c1 P + c2 Q + c3 O      (fz_recommend_t splits c1 by walk kind: staged pair walk or not)
+(Splitting memo and walk time into separate fits, or adding a per-tail-level term, fitted worse: the small-n
+rows are latency-bound.)  Prints the constants and, per case, the model's pick against the measured best t."""
 import json
 import sys
 
@@ -26,7 +27,7 @@ def cum(g, n):
     return c
 
 
-def features(g, n, t, mode):
+def feats(g, n, t, mode):
     d, L = len(g), len(g) - t
     R = cum(g, n)[n]
     P = cum(g[:L], n).sum()
@@ -42,30 +43,23 @@ def features(g, n, t, mode):
 
 def main(path):
     recs = [json.loads(x) for x in open(path) if x.strip()]
-    consts = {}
+    cs = {}
     for mode in ("materialize", "hash", "count"):
-        X, y = [], []
-        for r in recs:
-            if r["mode"] != mode:
-                continue
-            for t, us in r["step_us"].items():
-                f = features(tuple(r["gens"]), r["n"], int(t), mode)
-                X.append([v / (us * 1e-6) for v in f])
-                y.append(1.0)
+        X = [[v / (us * 1e-6) for v in feats(tuple(r["gens"]), r["n"], int(t), mode)]
+             for r in recs if r["mode"] == mode for t, us in r["step_us"].items()]
         if not X:
             continue
-        c, _ = nnls(np.array(X), np.array(y))
-        consts[mode] = c
-        print(f"{mode}: " + ", ".join(f"{v:.4g}" for v in c))
+        cs[mode], _ = nnls(np.array(X), np.ones(len(X)))
+        print(f"{mode}: " + ", ".join(f"{v:.4g}" for v in cs[mode]))
     worst = 1.0
     for r in recs:
-        c = consts[r["mode"]]
-        pred = {int(t): float(np.dot(c, features(tuple(r["gens"]), r["n"], int(t), r["mode"]))) for t in r["step_us"]}
+        mode = r["mode"]
+        pred = {int(t): float(np.dot(cs[mode], feats(tuple(r["gens"]), r["n"], int(t), mode))) for t in r["step_us"]}
         meas = {int(t): v for t, v in r["step_us"].items()}
         pick, best = min(pred, key=pred.get), min(meas, key=meas.get)
         ratio = meas[pick] / meas[best]
         worst = max(worst, ratio)
-        print(f"{r['case']:>22} {r['mode']:>11}: pick t={pick} ({meas[pick]:.1f} us), best t={best} "
+        print(f"{r['case']:>22} {mode:>11}: pick t={pick} ({meas[pick]:.1f} us), best t={best} "
               f"({meas[best]:.1f} us), ratio {ratio:.3f}")
     print(f"worst pick / best = {worst:.3f}")
 
