@@ -174,8 +174,8 @@ struct Sizing {
     Layout lay{};
 };
 
-constexpr uint64_t kCountRunCost = 64;     // COUNT pair-walk cost model (card lookups; measured, tools/count_tune.py): per innermost run
-constexpr uint64_t kCountOuterCost = 1024;  // ... and per outer prefix
+constexpr uint64_t kCountRunCost = 96;     // COUNT cost model (card lookups; measured, tools/count_tune.py): per innermost run
+constexpr uint64_t kCountOuterCost = 3072;  // ... and per outer prefix
 constexpr uint64_t kWordStreamRowsPerPrefix = 36;   // MATERIALIZE word stream from this many rows per prefix
 constexpr uint64_t kRows16MinBytes = 64ull << 20;   // u16 row copy: u32 rows above this (half the 126 MB L2)
 constexpr uint64_t kRows16MaxBytes = 96ull << 20;   //   ... and the copy below this
@@ -367,7 +367,9 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
     // u16 copy of the rows for the walks (k3_pack16) when the u32 rows overflow L2 but the u16 copy does not
     // and every coordinate is below 2^16 (C3 t = 3: 162 MB -> 81 MB)
     l.rows16 = 0;
-    if (z.fill_mode && rows_bytes > kRows16MinBytes && entries * 2ull * t <= kRows16MaxBytes) {
+    const char *r16e = getenv("FZ_ROWS16");   // 0: never build the u16 copy (A/B switch)
+    if (!(r16e && r16e[0] == '0') && z.fill_mode && rows_bytes > kRows16MinBytes &&
+        entries * 2ull * t <= kRows16MaxBytes) {
         uint32_t gmin = 0xffffffffu;
         for (int i = L; i < d; ++i) gmin = std::min(gmin, g[i]);
         if ((ltop - 1) / gmin < 65536) {
@@ -548,6 +550,10 @@ PairPlan pair_plan(const fz_layout *lay, uint64_t n)
     g.cs2 = (uint32_t)(((uint64_t)g.S3 % m + m - g2 % m) % m);
     g.is1 = e == 1 ? (uint32_t)((uint64_t)g.cs1 * inv % m) : 0;
     g.is2 = e == 1 ? (uint32_t)((uint64_t)g.cs2 * inv % m) : 0;
+    g.QD = (uint32_t)(32ull * g2 / m);
+    g.RD = (uint32_t)(32ull * g2 % m);
+    g.Fr = cmax == 0 ? (1u << 30) : (uint32_t)((u8 ? 255ull : 65535ull) / (2 * cmax));   // 2 cards per packed lane
+    if (g.Fr >= 4) g.Fr &= ~3u;
     P.on = true;
     P.u8 = u8;
     P.f0n = f0n;
@@ -764,7 +770,11 @@ fz_status launch_pairs_d(int t, const PairPlan &pp, const WalkArgs &a, const uin
 {
     if constexpr (T + 3 <= D) {
         if (t != T) return launch_pairs_d<D, T + 1>(t, pp, a, C, cardT, Rcol, s);
-        auto kern = pp.u8 ? fzk::k5_pairs<D, T, true> : fzk::k5_pairs<D, T, false>;
+        // FZ_COUNT_WALK=pairs / runs picks the COUNT kernel (default: runs)
+        const char *wk = getenv("FZ_COUNT_WALK");
+        const bool pairs = wk && wk[0] == 'p';
+        auto kern = pairs ? (pp.u8 ? fzk::k5_pairs<D, T, true> : fzk::k5_pairs<D, T, false>)
+                          : (pp.u8 ? fzk::k5_runs<D, T, true> : fzk::k5_runs<D, T, false>);
         FZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem));
         FZ_CUDA(launch_pdl(kern, dim3((unsigned)device_sms()), dim3(fzk::kCountThreads), pp.smem, s, a.G,
                            (uint64_t)a.n, a.hdr, C, (uint64_t)a.top, cardT, Rcol, pp.pg, pp.f0n));

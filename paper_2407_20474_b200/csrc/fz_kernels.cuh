@@ -1934,6 +1934,7 @@ struct PairGeo {
     // the common outer step (a_{L-3} decrements: R += g3, g3 = Q3 g2 + S3): column steps (mod m) and,
     // when e = 1, orbit-position steps (mod m) for the two outcomes of rmin + S3 >= g2
     uint32_t Q3, S3, cs1, cs2, is1, is2;
+    uint32_t QD, RD, Fr;                // k5_runs: 32 g2 = QD m + RD; flush period (vectors) of its packed sums
 };
 
 // x / d for any x < 2^32, d >= 1, from M = floor(2^32 / d) (d = 1: 2^32 - 1): umulhi underestimates the
@@ -2016,21 +2017,14 @@ __device__ __forceinline__ bool pair_locate(const uint64_t *__restrict__ Ct, uin
     return true;
 }
 
-template <int D, int T, bool U8>
-__global__ void __launch_bounds__(kCountThreads, 1)
-k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uint64_t top,
-         const uint32_t *__restrict__ cardT, uint64_t Rcol, PairGeo pg, uint32_t f0n)
+// the card image of the COUNT walks: stored column vp = coset s, orbit position j -> residue column
+// (s + (j mod m') Delta) mod m, R16 entries each (card[col + v m] for col + v m <= n, else 0)
+template <bool U8>
+__device__ __forceinline__ void stage_card_image(uint8_t *img, const PairGeo &pg, const uint32_t *__restrict__ cardT,
+                                                 uint64_t Rcol, uint64_t n64)
 {
-    constexpr int L = D - T;
-    static_assert(L >= 3, "pair walk: at least one outer coordinate");
-    constexpr int NO = L - 2;   // outer coordinates
-    constexpr uint32_t VE = U8 ? 16 : 8, VSH = U8 ? 4 : 3;   // entries per vector, log2
-    griddep_wait();   // PDL: the plan header (K4) and the count tables are complete and visible
-    extern __shared__ uint64_t f0s[];   // level-0 unrank column C_0[n - q g_0] (f0n entries), then the card image
-    for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Ct + (n64 - (uint64_t)q * G.g[0]));
-    uint8_t *img = reinterpret_cast<uint8_t *>(f0s + ((f0n + 1) & ~1u));
     const uint32_t m = pg.m;
-    {   // stage the card image: stored column vp = coset s, orbit position j -> column (s + (j mod m') Delta) mod m
+    {
         const uint32_t tot = pg.ncolv * pg.R16, per = pg.mp + pg.dup;
         for (uint32_t i0 = threadIdx.x; i0 < tot; i0 += 8 * blockDim.x) {
             uint32_t val[8];
@@ -2055,6 +2049,23 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
             }
         }
     }
+}
+
+template <int D, int T, bool U8>
+__global__ void __launch_bounds__(kCountThreads, 1)
+k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uint64_t top,
+         const uint32_t *__restrict__ cardT, uint64_t Rcol, PairGeo pg, uint32_t f0n)
+{
+    constexpr int L = D - T;
+    static_assert(L >= 3, "pair walk: at least one outer coordinate");
+    constexpr int NO = L - 2;   // outer coordinates
+    constexpr uint32_t VE = U8 ? 16 : 8, VSH = U8 ? 4 : 3;   // entries per vector, log2
+    griddep_wait();   // PDL: the plan header (K4) and the count tables are complete and visible
+    extern __shared__ uint64_t f0s[];   // level-0 unrank column C_0[n - q g_0] (f0n entries), then the card image
+    for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Ct + (n64 - (uint64_t)q * G.g[0]));
+    uint8_t *img = reinterpret_cast<uint8_t *>(f0s + ((f0n + 1) & ~1u));
+    const uint32_t m = pg.m;
+    stage_card_image<U8>(img, pg, cardT, Rcol, n64);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t g2 = G.g[L - 2];
@@ -2159,6 +2170,24 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
             uint32_t mR = 0, mA = 0, mrmin = 0, mcb = 0, mbx = 0, mby = 0, mpp = 0, mf = 0;
             bool mine = false;
             uint32_t filled = 0;
+            if (A / 2 + 1 - c >= 32) {   // common pass: all 32 lanes from the current outer prefix (uniform)
+                uint32_t bx = idx0 + c, by = idx0 + A + 32 * pg.mp - c - 31;
+                if (pg.dup) {
+                    bx -= div32(bx, pg.mp, pg.Mmp) * pg.mp;
+                    by -= div32(by, pg.mp, pg.Mmp) * pg.mp;
+                }
+                mine = true;
+                mR = R;
+                mA = A;
+                mrmin = rmin;
+                mcb = cb;
+                mbx = bx;
+                mby = by;
+                mpp = c;
+                filled = 32;
+                c += 32;
+                if (c == A / 2 + 1) live = advance();
+            }
             while (filled < 32 && live) {
                 const uint32_t P = A / 2 + 1;
                 const uint32_t take = (P - c < 32 - filled) ? P - c : 32 - filled;
@@ -2262,6 +2291,174 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
             if (tX) sum = add_prefix<U8>(lds128(xa - 16 * (NY - NX)), tX, sum);
             acc += sum;
         }
+    }
+    acc = warp_sum_u64(acc);
+    if (lane == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)acc);
+}
+
+// COUNT, lane-per-run variant of the same walk (k5_runs): inside an outer prefix lane l takes the runs
+// k = l, l + 32, .. <= A one after the other, stepping each run's remainder by 32 g2 without division
+// (q += QD, residue += RD); the 32 runs of a round sit in 32 consecutive stored columns (orbit order), each
+// lane reads vectors 0.. of its own column (the same index in every lane: conflict-free) and drops out
+// after its own length (divergent trip counts instead of k5_pairs' per-pass pair setup).  Same card image,
+// packed IADD3 sums (two per vector, flushed every Fr vectors), dp2a / dp4a selector tails, cost-rank
+// guided slices and slice ends as k5_pairs.
+template <int D, int T, bool U8>
+__global__ void __launch_bounds__(kCountThreads, 1)
+k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uint64_t top,
+        const uint32_t *__restrict__ cardT, uint64_t Rcol, PairGeo pg, uint32_t f0n)
+{
+    constexpr int L = D - T;
+    static_assert(L >= 3, "run walk: at least one outer coordinate");
+    constexpr int NO = L - 2;   // outer coordinates
+    constexpr uint32_t VE = U8 ? 16 : 8, VSH = U8 ? 4 : 3;   // entries per vector, log2
+    griddep_wait();   // PDL: the plan header (K4) and the count tables are complete and visible
+    extern __shared__ uint64_t f0s[];   // level-0 unrank column C_0[n - q g_0] (f0n entries), then the card image
+    for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Ct + (n64 - (uint64_t)q * G.g[0]));
+    uint8_t *img = reinterpret_cast<uint8_t *>(f0s + ((f0n + 1) & ~1u));
+    stage_card_image<U8>(img, pg, cardT, Rcol, n64);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t m = pg.m, g2 = G.g[L - 2];
+    const uint64_t shard_begin = hdr->shard_begin, shard_len = hdr->shard_len, nslices = hdr->nslices,
+                   gw = hdr->gss_warps, fl = hdr->slice_len, total = hdr->total_units;
+    const uint32_t per = pg.mp + pg.dup;
+    const uint32_t colB = pg.R16 * (U8 ? 1u : 2u);   // bytes per stored column
+    const uint32_t img_a = smem_addr(img);
+    const uint64_t *F0 = f0n ? f0s : nullptr;
+    const bool e1 = pg.e == 1;
+    uint64_t acc = 0;
+
+    for (;;) {
+        uint64_t si = 0;
+        if (lane == 0) si = atomicAdd(&hdr->next_slice, 1ull);
+        si = shfl_u64(si, 0);
+        if (si >= nslices) break;
+        const uint64_t b = shard_begin + gss_begin(si, shard_len, gw, fl),
+                       e = shard_begin + gss_begin(si + 1, shard_len, gw, fl);
+        if (b >= e) continue;
+        uint32_t o[NO], rj[NO + 1], oe[NO], re[NO + 1];
+        if (!pair_locate<NO>(Ct, top, G, n64, b, F0, pg, o, rj)) continue;
+        const bool to_stream_end = e >= total || !pair_locate<NO>(Ct, top, G, n64, e, F0, pg, oe, re);
+        auto at_end = [&]() -> bool {
+            if (to_stream_end) return false;
+            bool eq = true;
+#pragma unroll
+            for (int j = 0; j < NO; ++j) eq = eq && (o[j] == oe[j]);
+            return eq;
+        };
+        if (at_end()) continue;
+        uint32_t R = 0, A = 0, rmin = 0, col = 0, cb = 0, idx0 = 0;
+        auto orbit = [&]() {
+            const uint32_t s = col - div32(col, pg.e, pg.Me) * pg.e;
+            const uint32_t cp = div32(col - s, pg.e, pg.Me) * pg.inv;
+            idx0 = cp - div32(cp, pg.mp, pg.Mmp) * pg.mp;
+            cb = s * per;
+        };
+        auto load = [&]() {
+            R = rj[NO];
+            A = div32(R, g2, pg.Mg2);
+            rmin = R - A * g2;
+            col = rmin - div32(rmin, m, pg.Mm) * m;
+            if (e1) {
+                const uint32_t cp = col * pg.inv;
+                idx0 = cp - div32(cp, m, pg.Mm) * m;
+                cb = 0;
+            } else {
+                orbit();
+            }
+        };
+        auto advance = [&]() -> bool {
+            if (o[NO - 1] > 0) {
+                o[NO - 1] -= 1;
+                rj[NO] += G.g[NO - 1];
+                if (at_end()) return false;
+                R = rj[NO];
+                rmin += pg.S3;
+                A += pg.Q3;
+                const bool cy = rmin >= g2;
+                if (cy) {
+                    rmin -= g2;
+                    A += 1;
+                }
+                col += cy ? pg.cs2 : pg.cs1;
+                if (col >= m) col -= m;
+                if (e1) {
+                    idx0 += cy ? pg.is2 : pg.is1;
+                    if (idx0 >= m) idx0 -= m;
+                } else {
+                    orbit();
+                }
+                return true;
+            }
+            int i = -1;
+#pragma unroll
+            for (int j = 0; j < NO - 1; ++j)
+                if (o[j] > 0) i = j;
+            if (i < 0) return false;
+#pragma unroll
+            for (int j = 0; j < NO; ++j) {
+                if (j == i) o[j] -= 1;
+                if (j > i) o[j] = div32(rj[j], G.g[j], pg.Mg[j]);
+                if (j >= i) rj[j + 1] = rj[j] - o[j] * G.g[j];
+            }
+            if (at_end()) return false;
+            load();
+            return true;
+        };
+        load();
+        do {
+            // this outer prefix: lane l takes runs k = l, l + 32, ..; run k has remainder rmin + k g2
+            // (quotient q, residue rr mod m) and lies in stored column cb + orbit position idx0 + k
+            const uint32_t rk = rmin + (uint32_t)lane * g2;
+            uint32_t q = div32(rk, m, pg.Mm), rr = rk - q * m;
+            uint32_t base = idx0;   // orbit position of the round's first run, mod m'
+            for (uint32_t kb = 0; kb <= A; kb += 32) {
+                const uint32_t len = (kb + lane <= A) ? q + 1 : 0u;
+                uint32_t jp = base + lane;
+                if (!pg.dup) jp -= div32(jp, pg.mp, pg.Mmp) * pg.mp;
+                uint32_t a = img_a + (cb + jp) * colB;
+                const uint32_t N = len >> VSH;
+                uint32_t sum = 0, j = 0;
+                while (j < N) {
+                    const uint32_t je = (N - j < pg.Fr) ? N : j + pg.Fr;
+                    uint32_t a0 = 0, a1 = 0;
+#pragma unroll 1
+                    for (; j + 4 <= je; j += 4) {
+                        const uint4 w0 = lds128(a), w1 = lds128(a + 16), w2 = lds128(a + 32), w3 = lds128(a + 48);
+                        a0 += w0.x + w0.y;
+                        a1 += w0.z + w0.w;
+                        a0 += w1.x + w1.y;
+                        a1 += w1.z + w1.w;
+                        a0 += w2.x + w2.y;
+                        a1 += w2.z + w2.w;
+                        a0 += w3.x + w3.y;
+                        a1 += w3.z + w3.w;
+                        a += 64;
+                    }
+#pragma unroll 1
+                    for (; j < je; ++j) {
+                        const uint4 w0 = lds128(a);
+                        a0 += w0.x + w0.y;
+                        a1 += w0.z + w0.w;
+                        a += 16;
+                    }
+                    sum = unpack_add<U8>(a1, unpack_add<U8>(a0, sum));
+                }
+                const uint32_t tl = len & (VE - 1);
+                if (tl) sum = add_prefix<U8>(lds128(a), tl, sum);
+                acc += sum;
+                // next round: k += 32
+                q += pg.QD;
+                rr += pg.RD;
+                if (rr >= m) {
+                    rr -= m;
+                    q += 1;
+                }
+                base += 32;
+                if (pg.dup) base -= div32(base, pg.mp, pg.Mmp) * pg.mp;
+            }
+        } while (advance());
     }
     acc = warp_sum_u64(acc);
     if (lane == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)acc);

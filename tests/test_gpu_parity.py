@@ -184,11 +184,12 @@ def test_c3_count_hash(t, corc):
 
 
 # ---------------------------------------------------------------------- C4
-@pytest.mark.parametrize("t", [3, 2])
-def test_c4_count(t, corc):
+@pytest.mark.parametrize("t,walk", [(3, "runs"), (2, "runs"), (3, "pairs")])
+def test_c4_count(t, walk, corc, monkeypatch):
     """C4 count-only, t = 3 (u16 card image) and t = 2 (u8 image, 6.14e12 lookups): the pair walk's count ==
     the independent GF count (3 356 809 984 741), whole and over 2 / 8 shards, in bench.py's launch
-    configuration (BASELINE configs[3])."""
+    configuration (BASELINE configs[3]); both COUNT kernels (k5_runs default, k5_pairs via FZ_COUNT_WALK)."""
+    monkeypatch.setenv("FZ_COUNT_WALK", walk)
     memo = fz.memo_build(C4.gens, t, C4.n + 1, entries=False)
     want = corc.gf_count(C4.n, C4.gens)
     assert want == 3_356_809_984_741
@@ -202,12 +203,14 @@ def test_c4_count(t, corc):
         assert tot == want, k
 
 
+@pytest.mark.parametrize("walk", ["runs", "pairs"])
 @pytest.mark.parametrize("seed", range(32))
-def test_count_staged(seed, corc, monkeypatch):
+def test_count_staged(seed, walk, corc, monkeypatch):
     """COUNT with the card table staged in shared memory, forced on small walks (FZ_COUNT_SMEM=2):
-    the outer-prefix walk (L >= 3) and the run-per-lane walk (L = 2) give the oracle's count, whole
+    the COUNT kernels for L >= 3 (k5_runs, k5_pairs) and the run-per-lane walk (L = 2) give the oracle's count, whole
     and cut into 2, 3 and 7 shards, for every t."""
     monkeypatch.setenv("FZ_COUNT_SMEM", "2")
+    monkeypatch.setenv("FZ_COUNT_WALK", walk)
     for g, n in (random_instance(seed)[:2], random_instance_mid(seed)[:2]):
         cnt = corc.gf_count(n, g)
         for t in range(0, len(g)):
