@@ -179,7 +179,8 @@ def roofline(W, plan, k5_ms: float, rows_local: int, sm_max_mhz, props, world: i
         U = leading_prefixes(g, n, d - t)
         units = U / W["nshards"]
         peak = sms * 128 / card_bytes * clk
-        r = {"kernel": f"k5_pairs<{d},{t},{'u8' if card_bytes == 1 else 'u16'}>" if walk == "count_pairs"
+        kname = {"count_staged": "k5_runs", "count_pairs": "k5_pairs"}.get(walk)
+        r = {"kernel": f"{kname}<{d},{t},{'u8' if card_bytes == 1 else 'u16'}>" if kname
              else f"k5_walk<{d},{t},count>", "bound": "smem",
              "achieved": units / (k5_ms / 1e3), "peak": peak, "unit": "card lookups/s",
              "peak_source": (f"derived: {sms} SMs x 128 B/clk shared-memory crossbar (B300_MICROARCH.md LDS/STS) / "

@@ -198,10 +198,12 @@ void fz_plan_free(fz_plan *p);
  *   FZ_WALK_ROWS         k5_walk over memo blocks (MATERIALIZE / HASH, full memo)
  *   FZ_WALK_DEEP         k5_deep (partial memo, n >= memo_top)
  *   FZ_WALK_TABLE        k5_table (t = d: Z(n) is the block Memo[n])
- *   FZ_WALK_COUNT_PAIRS  k5_pairs (COUNT, L >= 3: staged card image, pairs of innermost runs per lane)
+ *   FZ_WALK_COUNT_STAGED k5_runs (COUNT, L >= 3: staged card image, one innermost run per lane; default)
+ *   FZ_WALK_COUNT_PAIRS  k5_pairs (the same walk with a pair of runs per lane; FZ_COUNT_WALK=pairs)
  *   FZ_WALK_COUNT_RUNS   k5_walk COUNT (L <= 2, or a card table that cannot be staged)
  * card_bytes: bytes per card lookup of the COUNT walk (1 = u8 image, 2 = u16 image, 4 = u32 table; 0 otherwise). */
-enum { FZ_WALK_ROWS = 0, FZ_WALK_DEEP = 1, FZ_WALK_TABLE = 2, FZ_WALK_COUNT_PAIRS = 3, FZ_WALK_COUNT_RUNS = 4 };
+enum { FZ_WALK_ROWS = 0, FZ_WALK_DEEP = 1, FZ_WALK_TABLE = 2, FZ_WALK_COUNT_PAIRS = 3, FZ_WALK_COUNT_RUNS = 4,
+       FZ_WALK_COUNT_STAGED = 5 };
 fz_status fz_plan_walk(const fz_plan *p, int *kind, int *card_bytes);
 
 /* This plan's shard as computed on the device: first global row, row count,

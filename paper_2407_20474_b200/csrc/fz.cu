@@ -472,6 +472,13 @@ fzk::ProgGens make_prog(const uint32_t *g, int d)
 
 constexpr uint64_t kPairSmemMax = 220 * 1024;   // dynamic shared memory of one k5_pairs CTA (one per SM)
 
+// the COUNT kernel of the staged walk: k5_runs (default) or k5_pairs (FZ_COUNT_WALK=pairs)
+bool count_walk_pairs()
+{
+    const char *wk = getenv("FZ_COUNT_WALK");
+    return wk && wk[0] == 'p';
+}
+
 PairPlan pair_plan(const fz_layout *lay, uint64_t n)
 {
     PairPlan P;
@@ -770,9 +777,7 @@ fz_status launch_pairs_d(int t, const PairPlan &pp, const WalkArgs &a, const uin
 {
     if constexpr (T + 3 <= D) {
         if (t != T) return launch_pairs_d<D, T + 1>(t, pp, a, C, cardT, Rcol, s);
-        // FZ_COUNT_WALK=pairs / runs picks the COUNT kernel (default: runs)
-        const char *wk = getenv("FZ_COUNT_WALK");
-        const bool pairs = wk && wk[0] == 'p';
+        const bool pairs = count_walk_pairs();
         auto kern = pairs ? (pp.u8 ? fzk::k5_pairs<D, T, true> : fzk::k5_pairs<D, T, false>)
                           : (pp.u8 ? fzk::k5_runs<D, T, true> : fzk::k5_runs<D, T, false>);
         FZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem));
@@ -1384,7 +1389,7 @@ fz_status fz_plan_walk(const fz_plan *p, int *kind, int *card_bytes)
     int k = FZ_WALK_ROWS, cb = 0;
     if (p->mode == FZ_COUNT && z.L > 0) {
         if (p->pp.on) {
-            k = FZ_WALK_COUNT_PAIRS;
+            k = count_walk_pairs() ? FZ_WALK_COUNT_PAIRS : FZ_WALK_COUNT_STAGED;
             cb = p->pp.u8 ? 1 : 2;
         } else {
             k = FZ_WALK_COUNT_RUNS;

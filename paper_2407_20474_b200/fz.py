@@ -262,7 +262,7 @@ class Plan:
             self._shard = (rb.value, rl.value, ns.value)
         return self._shard
 
-    WALKS = {0: "rows", 1: "deep", 2: "table", 3: "count_pairs", 4: "count_runs"}
+    WALKS = {0: "rows", 1: "deep", 2: "table", 3: "count_pairs", 4: "count_runs", 5: "count_staged"}
 
     def walk(self):
         """(kernel kind, bytes per card lookup) of this plan's enumeration (fz_plan_walk)."""

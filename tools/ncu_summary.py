@@ -3,7 +3,7 @@
   python tools/ncu_summary.py launches <launches.csv> <out.md>     # --metrics gpu__time_duration.sum list
   python tools/ncu_summary.py full <report.ncu-rep | raw.csv> <out.md> [key]  # --set full capture (one or more kernels)
 
-`full` also merges {key: {dram_bytes_per_launch, ...}} into profiles/k5_traffic.json.
+`full` also merges {key: {dram_bytes_per_launch, warp_inst_per_launch, ...}} into profiles/k5_counters.json.
 """
 import csv
 import io
@@ -56,7 +56,9 @@ def full(rep, out, key=None):
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct", "launch__grid_size", "launch__block_size",
             "smsp__inst_executed.sum", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
-            "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
+            "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+            "smsp__inst_executed_op_shared_ld.sum", "sm__cycles_active.avg", "sm__cycles_elapsed.avg"]
     idx = {h: i for i, h in enumerate(hdr)}
     lines = [f"# ncu --set full: `{os.path.basename(rep)}`", ""]
     summ = {}
@@ -80,14 +82,19 @@ def full(rep, out, key=None):
             x, u = v
             x = float(x.replace(",", ""))
             return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
-        k5 = [v for n, v in summ.items() if "k5_walk" in n]
+        k5 = [v for n, v in summ.items() if any(k in n for k in ("k5_walk", "k5_runs", "k5_pairs"))]
         if k5:
             v = k5[0]
             dram = tobytes(v["dram__bytes_read.sum"]) + tobytes(v["dram__bytes_write.sum"])
-            p = os.path.join(ROOT, "profiles", "k5_traffic.json")
+            # bench.py reads profiles/k5_counters.json (per-launch DRAM bytes and warp instructions of each
+            # leg's dominant kernel at the kernel version captured)
+            p = os.path.join(ROOT, "profiles", "k5_counters.json")
             cur = json.load(open(p)) if os.path.exists(p) else {}
             cur[key] = {"dram_bytes_per_launch": dram, "dram_read": tobytes(v["dram__bytes_read.sum"]),
-                        "dram_write": tobytes(v["dram__bytes_write.sum"]), "source": os.path.basename(out)}
+                        "dram_write": tobytes(v["dram__bytes_write.sum"]),
+                        "warp_inst_per_launch": float(v["smsp__inst_executed.sum"][0].replace(",", "")),
+                        "duration_ns": float(v["gpu__time_duration.sum"][0].replace(",", "")),
+                        "source": os.path.basename(out)}
             json.dump(cur, open(p, "w"), indent=1)
 
 

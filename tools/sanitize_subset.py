@@ -35,5 +35,27 @@ for g, n, t in [((13, 37, 38, 40, 41), 600, 1), ((3, 5, 8, 11), 200, 1), ((3, 5,
     cnt = C.gf_count(n, g)
     for ns in (1, 3):
         bad += sum(fz.enumerate(memo, n, "count", shard=s, nshards=ns)[1] for s in range(ns)) != cnt
+for walk in ("runs", "pairs"):   # both COUNT kernels of L >= 3
+    os.environ["FZ_COUNT_WALK"] = walk
+    for g, n, t in [((13, 37, 38, 40, 41), 600, 2), ((3, 5, 8, 11, 13), 200, 1), ((97, 98, 99, 100, 101), 900, 2)]:
+        memo = fz.memo_build(g, t, n + 1, entries=False)
+        cnt = C.gf_count(n, g)
+        for ns in (1, 3):
+            bad += sum(fz.enumerate(memo, n, "count", shard=s, nshards=ns)[1] for s in range(ns)) != cnt
 os.environ["FZ_COUNT_SMEM"] = ""
+os.environ["FZ_COUNT_WALK"] = ""
+# the MATERIALIZE word stream (odd d, long rounds) and the end-to-end output ring (tiny slots: many chunks)
+os.environ["FZ_WORD_STREAM"] = "1"
+for g, n, t in [((13, 37, 38, 40, 41), 900, 3), ((13, 37, 38, 40, 41, 42, 43, 44, 45), 600, 5)]:
+    memo = fz.memo_build(g, t, n + 1)
+    want, cnt, h = C.enumerate(n, g)
+    out, r, _ = fz.enumerate(memo, n, "materialize")
+    bad += not np.array_equal(out.cpu().numpy().view(np.uint32).reshape(-1, len(g))[:r], want.reshape(-1, len(g)))
+os.environ["FZ_WORD_STREAM"] = ""
+import torch  # noqa: E402
+g, n, t = (13, 37, 38, 40), 3000, 2
+want, cnt, h = C.enumerate(n, g)
+host = torch.empty((cnt, len(g)), dtype=torch.int32).pin_memory()
+r, _ = fz.run_host(g, t, n, "materialize", host, ring_bytes=4096)
+bad += (r != cnt) or not np.array_equal(host.numpy().view(np.uint32), want.reshape(-1, len(g)))
 print("sanitize subset:", "OK" if bad == 0 else f"{bad} FAILURES")
