@@ -2413,15 +2413,16 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
             const uint32_t rk = rmin + (uint32_t)lane * g2;
             uint32_t q = div32(rk, m, pg.Mm), rr = rk - q * m;
             uint32_t base = idx0;   // orbit position of the round's first run, mod m'
+            // the longest run of this outer prefix (run A) has (R / m + 1) / VE full vectors: one flush chunk of
+            // the packed sums suffices when that is at most Fr (uniform; always on C4)
+            const bool one_chunk = ((div32(R, m, pg.Mm) + 1) >> VSH) <= pg.Fr;
             for (uint32_t kb = 0; kb <= A; kb += 32) {
                 const uint32_t len = (kb + lane <= A) ? q + 1 : 0u;
-                uint32_t jp = base + lane;
-                if (!pg.dup) jp -= div32(jp, pg.mp, pg.Mmp) * pg.mp;
-                uint32_t a = img_a + (cb + jp) * colB;
+                const uint32_t jp = base + lane;   // < m' + 31 with duplicates, reduced below without
+                uint32_t a = img_a + (cb + (pg.dup ? jp : jp - div32(jp, pg.mp, pg.Mmp) * pg.mp)) * colB;
                 const uint32_t N = len >> VSH;
                 uint32_t sum = 0, j = 0;
-                while (j < N) {
-                    const uint32_t je = (N - j < pg.Fr) ? N : j + pg.Fr;
+                auto span = [&](uint32_t je) {   // vectors [j, je) of this lane's run into the packed sums
                     uint32_t a0 = 0, a1 = 0;
 #pragma unroll 1
                     for (; j + 4 <= je; j += 4) {
@@ -2436,14 +2437,31 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
                         a1 += w3.z + w3.w;
                         a += 64;
                     }
-#pragma unroll 1
-                    for (; j < je; ++j) {
+                    // the remaining 0..3 vectors: predicated loads (no divergent 1-step loop)
+                    const uint32_t r = je - j;
+                    if (r > 0) {
                         const uint4 w0 = lds128(a);
                         a0 += w0.x + w0.y;
                         a1 += w0.z + w0.w;
-                        a += 16;
                     }
+                    if (r > 1) {
+                        const uint4 w1 = lds128(a + 16);
+                        a0 += w1.x + w1.y;
+                        a1 += w1.z + w1.w;
+                    }
+                    if (r > 2) {
+                        const uint4 w2 = lds128(a + 32);
+                        a0 += w2.x + w2.y;
+                        a1 += w2.z + w2.w;
+                    }
+                    a += 16 * r;
+                    j = je;
                     sum = unpack_add<U8>(a1, unpack_add<U8>(a0, sum));
+                };
+                if (one_chunk) {
+                    span(N);
+                } else {
+                    while (j < N) span((N - j < pg.Fr) ? N : j + pg.Fr);
                 }
                 const uint32_t tl = len & (VE - 1);
                 if (tl) sum = add_prefix<U8>(lds128(a), tl, sum);
@@ -2456,7 +2474,13 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
                     q += 1;
                 }
                 base += 32;
-                if (pg.dup) base -= div32(base, pg.mp, pg.Mmp) * pg.mp;
+                if (pg.dup) {   // base mod m' (one subtraction when m' >= 32)
+                    if (pg.mp >= 32) {
+                        if (base >= pg.mp) base -= pg.mp;
+                    } else {
+                        base -= div32(base, pg.mp, pg.Mmp) * pg.mp;
+                    }
+                }
             }
         } while (advance());
     }

@@ -93,7 +93,9 @@ def full(rep, out, key=None):
             cur[key] = {"dram_bytes_per_launch": dram, "dram_read": tobytes(v["dram__bytes_read.sum"]),
                         "dram_write": tobytes(v["dram__bytes_write.sum"]),
                         "warp_inst_per_launch": float(v["smsp__inst_executed.sum"][0].replace(",", "")),
-                        "duration_ns": float(v["gpu__time_duration.sum"][0].replace(",", "")),
+                        "duration_ns": float(v["gpu__time_duration.sum"][0].replace(",", "")) *
+                        {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(
+                            v["gpu__time_duration.sum"][1], 1),
                         "source": os.path.basename(out)}
             json.dump(cur, open(p, "w"), indent=1)
 

@@ -45,17 +45,30 @@ def check(g, n):
                 if not ok:
                     stats["failures"] += 1
                     print("FAIL", g, n, t, top, ns, tot, ct, cnt, hex(hs), hex(h), flush=True)
-    # COUNT with the card table staged in shared memory (forced)
+    # COUNT with the card table staged in shared memory (forced), both L >= 3 kernels (k5_runs, k5_pairs)
     os.environ["FZ_COUNT_SMEM"] = "2"
-    for t in range(0, d):
-        memo = fz.memo_build(g, t, n + 1, entries=False)
-        for ns in (1, 3):
-            ct = sum(fz.enumerate(memo, n, "count", shard=s, nshards=ns)[1] for s in range(ns))
-            stats["checks"] += 1
-            if ct != cnt:
-                stats["failures"] += 1
-                print("FAIL staged count", g, n, t, ns, ct, cnt, flush=True)
+    for walk in ("runs", "pairs"):
+        os.environ["FZ_COUNT_WALK"] = walk
+        for t in range(0, d):
+            memo = fz.memo_build(g, t, n + 1, entries=False)
+            for ns in (1, 3, 7):
+                ct = sum(fz.enumerate(memo, n, "count", shard=s, nshards=ns)[1] for s in range(ns))
+                stats["checks"] += 1
+                if ct != cnt:
+                    stats["failures"] += 1
+                    print("FAIL staged count", walk, g, n, t, ns, ct, cnt, flush=True)
     os.environ["FZ_COUNT_SMEM"] = ""
+    os.environ["FZ_COUNT_WALK"] = ""
+    # MATERIALIZE as a word stream (forced on, every t): rows element by element
+    os.environ["FZ_WORD_STREAM"] = "1"
+    for t in range(1, d):
+        memo = fz.memo_build(g, t, n + 1)
+        out, rows, _ = fz.enumerate(memo, n, "materialize")
+        stats["checks"] += 1
+        if rows != cnt or not np.array_equal(out.cpu().numpy().view(np.uint32).reshape(-1, d)[:rows], want):
+            stats["failures"] += 1
+            print("FAIL word stream", g, n, t, flush=True)
+    os.environ["FZ_WORD_STREAM"] = ""
 
 
 for fam, gen in (("random", random_instance), ("mid", random_instance_mid)):
@@ -69,5 +82,5 @@ for fam, gen in (("random", random_instance), ("mid", random_instance_mid)):
     stats["instances"] += n_inst
     print(f"{fam}: seeds {first}..{first + n_inst - 1} checked", flush=True)
 print(f"parity stress: {stats['instances']} instances, {stats['checks']} checks (every t, full + partial memos, "
-      f"1-4 shards, materialize/count/hash, staged count), {stats['failures']} failures, "
+      f"1-4 shards, materialize/count/hash, staged count with both kernels, word stream), {stats['failures']} failures, "
       f"{time.time() - t0:.0f} s", flush=True)
