@@ -1512,6 +1512,17 @@ struct BlockInfo {      // one non-empty memo block of the current warp round (1
     uint32_t v;         // innermost leading coordinate a_L of the block
 };
 
+__device__ __forceinline__ BlockInfo lds_block_info(uint32_t a)
+{
+    uint32_t x, y, z, w;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a));
+    BlockInfo b;
+    b.memo_row = ((uint64_t)y << 32) | x;
+    b.start = z;
+    b.v = w;
+    return b;
+}
+
 constexpr int kWalkThreads = 256;
 constexpr int kCountThreads = 1024;   // COUNT walk: one CTA per SM shares one staged card table
 template <int MODE>
@@ -1573,6 +1584,10 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     const uint64_t *__restrict__ offT = wt.offT;
     uint64_t acc_rows = 0, acc_hash = 0;
     BlockInfo *bi = binfo[wib];
+    // 32-bit shared address of this warp's block list, read back with ld.shared (keeps the compiler from
+    // re-deriving the generic shared window -- S2R TID / CgaCtaId -- for every 32-row chunk)
+    uint32_t bi_sa;   // (through a volatile move: the compiler keeps it in a register instead of recomputing it)
+    asm volatile("mov.b32 %0, %1;" : "=r"(bi_sa) : "r"(smem_addr(binfo[wib])));
     const uint32_t cgq = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] / m : 0, cgr = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] % m : 0;
 
     (void)gw;
@@ -1800,7 +1815,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                         const int e = before + __popc(M & lm_le);   // owner: the last block starting at or before q
                         before += __popc(M);
                         if (ok[u]) {
-                            const BlockInfo info = bi[e];
+                            const BlockInfo info = lds_block_info(bi_sa + 16u * (uint32_t)e);
 #pragma unroll
                             for (int j = 0; j < L - 1; ++j) wv[u][j] = a[j];
                             wv[u][L - 1] = info.v;
