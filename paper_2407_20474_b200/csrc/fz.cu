@@ -176,7 +176,7 @@ struct Sizing {
 
 constexpr uint64_t kCountRunCost = 96;     // COUNT cost model (card lookups; measured, tools/count_tune.py): per innermost run
 constexpr uint64_t kCountOuterCost = 3072;  // ... and per outer prefix
-constexpr uint64_t kWordStreamRowsPerPrefix = 36;   // MATERIALIZE word stream from this many rows per prefix
+constexpr uint64_t kWordStreamRowsPerPrefix = 8;    // MATERIALIZE word stream from this many rows per prefix
 constexpr uint64_t kRows16MinBytes = 64ull << 20;   // u16 row copy: u32 rows above this (half the 126 MB L2)
 constexpr uint64_t kRows16MaxBytes = 96ull << 20;   //   ... and the copy below this
 constexpr uint64_t kSmemMax = 220 * 1024;   // dynamic shared memory budget of the ring fill
@@ -744,27 +744,28 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     // not depend on n; the attribute must allow that size for the occupancy query (static shared memory --
     // the MATERIALIZE word-stream staging -- plus the dynamic part may pass 48 KB)
     const size_t smem_q = std::max<size_t>(smem, 4096 * 8);
-    FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fzk::k5_walk<D, T, MODE>, fzk::walk_threads<MODE>(),
-                                                      smem_q) != cudaSuccess ||
-        per_sm < 1) {
-        cudaGetLastError();
-        per_sm = 1;
-    }
-    per_sm = std::min(per_sm, 8);
-    bool m16 = false;
-    if constexpr (MODE == FZ_HASH) m16 = a.wt.memo16 != nullptr;
-    if constexpr (MODE == FZ_HASH) if (m16) {   // the u16 copy of the rows (same grid: same registers and smem)
-        FZ_CUDA(cudaFuncSetAttribute(fzk::k5_walk<D, T, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_q));
-        FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE, true>, dim3((unsigned)(device_sms() * per_sm)),
-                           dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
-                           a.wt, a.out, (uint64_t)a.cap, (uint64_t)a.row_base, f0n, c16R));
-    }
-    if (!m16) {
-        FZ_CUDA(launch_pdl(fzk::k5_walk<D, T, MODE>, dim3((unsigned)(device_sms() * per_sm)),
-                           dim3(fzk::walk_threads<MODE>()), smem, s, a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top,
-                           a.wt, a.out, (uint64_t)a.cap, (uint64_t)a.row_base, f0n, c16R));
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q);
+        if (e != cudaSuccess) return e;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fzk::walk_threads<MODE>(), smem_q) !=
+                cudaSuccess ||
+            per_sm < 1) {
+            cudaGetLastError();
+            per_sm = 1;
+        }
+        per_sm = std::min(per_sm, 8);
+        return launch_pdl(kern, dim3((unsigned)(device_sms() * per_sm)), dim3(fzk::walk_threads<MODE>()), smem, s,
+                          a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top, a.wt, a.out, (uint64_t)a.cap,
+                          (uint64_t)a.row_base, f0n, c16R);
+    };
+    if constexpr (MODE == FZ_HASH) {
+        if (a.wt.memo16) FZ_CUDA(go(fzk::k5_walk<D, T, MODE, true>));   // the u16 copy of the rows
+        else FZ_CUDA(go(fzk::k5_walk<D, T, MODE>));
+    } else if constexpr (MODE == FZ_MATERIALIZE && (D % 4) != 0) {
+        if (a.wt.word_stream) FZ_CUDA(go(fzk::k5_walk<D, T, MODE, false, true>));   // the word-stream variant
+        else FZ_CUDA(go(fzk::k5_walk<D, T, MODE>));
+    } else {
+        FZ_CUDA(go(fzk::k5_walk<D, T, MODE>));
     }
     ++g_launches;
     return cuda_check("k5_walk");
@@ -1010,10 +1011,15 @@ fz_status make_layout(const uint32_t *gens, int d, int t, uint64_t top, int with
     if (!lay) return fail(FZ_ECAP, "host allocation failed");
     for (int i = 0; i < d; ++i) lay->g[i] = gens[i];
     lay->with_entries = with_entries ? 1 : 0;
-    if ((st = host_tables(gens, d, d - t, top, lay->H)) ||
-        (st = size_memo(gens, d, t, top, memo_top, with_entries, lay->H, lay->z))) {
+    try {   // (host vectors: a failed allocation is FZ_ECAP, never an exception through the C ABI)
+        if ((st = host_tables(gens, d, d - t, top, lay->H)) ||
+            (st = size_memo(gens, d, t, top, memo_top, with_entries, lay->H, lay->z))) {
+            delete lay;
+            return st;
+        }
+    } catch (const std::bad_alloc &) {
         delete lay;
-        return st;
+        return fail(FZ_ECAP, "host sizing tables for top=%llu do not fit host memory", (unsigned long long)top);
     }
     *out = lay;
     return FZ_OK;
@@ -1448,7 +1454,7 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
     }
     a.wt.card64 = m->S + (uint64_t)z.L * z.top;
     {   // d not a multiple of 4: rows leave as a 16-B word stream when the warp rounds are long (measured on
-        // Table 1 rows: it pays from ~36 rows per leading prefix); FZ_WORD_STREAM=0/1 forces
+        // Table 1 rows: it pays from ~8 rows per leading prefix); FZ_WORD_STREAM=0/1 forces
         const char *e = getenv("FZ_WORD_STREAM");
         const uint64_t P = m->lay->H.W.empty() ? 0 : m->lay->H.W[p->n];
         const bool long_rounds = P && m->lay->H.S[p->n] >= kWordStreamRowsPerPrefix * P;

@@ -1541,8 +1541,8 @@ struct WalkTables {
 };
 
 
-template <int D, int T, int MODE, bool M16 = false>
-__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : 2)))
+template <int D, int T, int MODE, bool M16 = false, bool WS = false>
+__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : (WS ? 3 : 2))))
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
@@ -1564,7 +1564,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     static_assert(L >= 1, "at least one leading coordinate");
     __shared__ BlockInfo binfo[MODE == FZ_COUNT ? 1 : kWalkThreads / 32][32];   // MAT/HASH block lists
     // MATERIALIZE with d not a multiple of 4: per-warp staging of 128 rows as a word stream (+ 3 words of phase)
-    constexpr bool kWordStream = MODE == FZ_MATERIALIZE && (D % 4) != 0;
+    constexpr bool kWordStream = WS && MODE == FZ_MATERIALIZE && (D % 4) != 0;
     constexpr int kUnr = (MODE == FZ_MATERIALIZE) ? 4 : 2;   // 32-row chunks per store group (d >= 7 with 2: slower)
     __shared__ __align__(16) uint32_t wsb[kWordStream ? kWalkThreads / 32 : 1][kWordStream ? 32 * kUnr * D + 4 : 1];
     const int lane = threadIdx.x & 31, wib = (MODE == FZ_COUNT) ? 0 : threadIdx.x >> 5;
@@ -1802,6 +1802,52 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 asm("mov.u32 %0, %%lanemask_le;" : "=r"(lm_le));
                 int before = -1;   // block starts before the chunk, minus one
                 for (uint32_t q0 = 0; q0 < use; q0 += 32 * UNR) {
+                    if constexpr (kWordStream) {
+                        // d not a multiple of 4 (WS variant): the warp's rows [q0, q0 + nr) are one contiguous run
+                        // of nr d words; each row goes to shared memory (at the 16-B phase of its global
+                        // address) as soon as its memo tail is loaded, then the aligned middle leaves as 16-B
+                        // vectors (scalar head and tail words)
+                        const uint32_t nr = (use - q0 < 32u * UNR) ? use - q0 : 32u * UNR;
+                        const uint64_t G0 = (outpos + q0) * (uint64_t)D;        // first word (shard-relative)
+                        const uint32_t sft = (uint32_t)(((uintptr_t)(out + G0) >> 2) & 3);
+                        uint32_t *sb = wsb[wib] + sft;
+#pragma unroll
+                        for (int u = 0; u < UNR; ++u) {
+                            const uint32_t qb = q0 + 32 * u;
+                            uint32_t bit;
+                            asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(rel - qb));
+                            const unsigned M = __reduce_or_sync(kFull, bit);
+                            const uint32_t q = qb + lane;
+                            const int e = before + __popc(M & lm_le);
+                            before += __popc(M);
+                            if (q < use) {
+                                const BlockInfo info = lds_block_info(bi_sa + 16u * (uint32_t)e);
+                                uint32_t *rw = sb + (32 * u + lane) * D;
+#pragma unroll
+                                for (int j = 0; j < L - 1; ++j) rw[j] = a[j];
+                                rw[L - 1] = info.v;
+                                if constexpr (T > 0) {
+                                    uint32_t tw[T];
+                                    load_tail<T>(reinterpret_cast<const uint32_t *>(info.memo_row + (uint64_t)q * (4 * T)),
+                                                 tw);
+#pragma unroll
+                                    for (int j = 0; j < T; ++j) rw[L + j] = tw[j];
+                                }
+                            }
+                        }
+                        __syncwarp();
+                        const uint32_t W = nr * D, head = ((4 - sft) & 3) < W ? ((4 - sft) & 3) : W;
+                        const uint32_t nv = (W - head) >> 2, tail0 = head + 4 * nv;
+                        uint32_t *og = out + G0;
+                        if ((uint32_t)lane < head) st_cs_u32(og + lane, sb[lane]);
+                        for (uint32_t v = lane; v < nv; v += 32) {
+                            const uint4 w4 = *reinterpret_cast<const uint4 *>(sb + head + 4 * v);
+                            st_cs_v4(og + head + 4 * v, w4);
+                        }
+                        if ((uint32_t)lane < W - tail0) st_cs_u32(og + tail0 + lane, sb[tail0 + lane]);
+                        __syncwarp();
+                        continue;
+                    }
                     uint32_t wv[UNR][D];
                     bool ok[UNR];
 #pragma unroll
@@ -1832,32 +1878,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                             }
                         }
                     }
-                    if (kWordStream && wt.word_stream) {
-                        // d not a multiple of 4: the warp's rows [q0, q0 + nr) are one contiguous run of nr d
-                        // words; stage them in shared memory at the 16-B phase of their global address and
-                        // write the aligned middle as 16-B vectors (scalar head and tail words)
-                        const uint32_t nr = (use - q0 < 32u * UNR) ? use - q0 : 32u * UNR;
-                        const uint64_t G0 = (outpos + q0) * (uint64_t)D;        // first word (shard-relative)
-                        const uint32_t sft = (uint32_t)(((uintptr_t)(out + G0) >> 2) & 3);
-                        uint32_t *sb = wsb[wib] + sft;
-#pragma unroll
-                        for (int u = 0; u < UNR; ++u) {
-                            if (!ok[u]) continue;
-#pragma unroll
-                            for (int j = 0; j < D; ++j) sb[(32 * u + lane) * D + j] = wv[u][j];
-                        }
-                        __syncwarp();
-                        const uint32_t W = nr * D, head = ((4 - sft) & 3) < W ? ((4 - sft) & 3) : W;
-                        const uint32_t nv = (W - head) >> 2, tail0 = head + 4 * nv;
-                        uint32_t *og = out + G0;
-                        if ((uint32_t)lane < head) st_cs_u32(og + lane, sb[lane]);
-                        for (uint32_t v = lane; v < nv; v += 32) {
-                            const uint4 w4 = *reinterpret_cast<const uint4 *>(sb + head + 4 * v);
-                            st_cs_v4(og + head + 4 * v, w4);
-                        }
-                        if ((uint32_t)lane < W - tail0) st_cs_u32(og + tail0 + lane, sb[tail0 + lane]);
-                        __syncwarp();
-                    } else {
+                    {
                         uint32_t *ob = out + (outpos + q0 + lane) * (uint64_t)D;   // chunk u at ob + 32 u D
 #pragma unroll
                         for (int u = 0; u < UNR; ++u) {
@@ -2082,13 +2103,15 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
     const uint32_t m = pg.m;
     stage_card_image<U8>(img, pg, cardT, Rcol, n64);
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    int lane;
+    asm volatile("mov.b32 %0, %1;" : "=r"(lane) : "r"((int)(threadIdx.x & 31)));
     const uint32_t g2 = G.g[L - 2];
     const uint64_t shard_begin = hdr->shard_begin, shard_len = hdr->shard_len, nslices = hdr->nslices,
                    gw = hdr->gss_warps, fl = hdr->slice_len, total = hdr->total_units;
     const uint32_t per = pg.mp + pg.dup;
     const uint32_t colB = pg.R16 * (U8 ? 1u : 2u);   // bytes per stored column
-    const uint32_t img_a = smem_addr(img);
+    uint32_t img_a;   // kept in a register (a volatile move): no per-round S2R TID / CgaCtaId re-derivation
+    asm volatile("mov.b32 %0, %1;" : "=r"(img_a) : "r"(smem_addr(img)));
     const uint64_t *F0 = f0n ? f0s : nullptr;
     const bool e1 = pg.e == 1;
     uint64_t acc = 0;
@@ -2333,13 +2356,15 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
     uint8_t *img = reinterpret_cast<uint8_t *>(f0s + ((f0n + 1) & ~1u));
     stage_card_image<U8>(img, pg, cardT, Rcol, n64);
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    int lane;
+    asm volatile("mov.b32 %0, %1;" : "=r"(lane) : "r"((int)(threadIdx.x & 31)));
     const uint32_t m = pg.m, g2 = G.g[L - 2];
     const uint64_t shard_begin = hdr->shard_begin, shard_len = hdr->shard_len, nslices = hdr->nslices,
                    gw = hdr->gss_warps, fl = hdr->slice_len, total = hdr->total_units;
     const uint32_t per = pg.mp + pg.dup;
     const uint32_t colB = pg.R16 * (U8 ? 1u : 2u);   // bytes per stored column
-    const uint32_t img_a = smem_addr(img);
+    uint32_t img_a;   // kept in a register (a volatile move): no per-round S2R TID / CgaCtaId re-derivation
+    asm volatile("mov.b32 %0, %1;" : "=r"(img_a) : "r"(smem_addr(img)));
     const uint64_t *F0 = f0n ? f0s : nullptr;
     const bool e1 = pg.e == 1;
     uint64_t acc = 0;
