@@ -560,6 +560,8 @@ PairPlan pair_plan(const fz_layout *lay, uint64_t n)
     g.QD = (uint32_t)(32ull * g2 / m);
     g.RD = (uint32_t)(32ull * g2 % m);
     g.Fr = cmax == 0 ? (1u << 30) : (uint32_t)((u8 ? 255ull : 65535ull) / (2 * cmax));   // 2 cards per packed lane
+    g.beta = z.beta;
+    g.gamma = z.gamma;
     if (g.Fr >= 4) g.Fr &= ~3u;
     P.on = true;
     P.u8 = u8;
@@ -771,37 +773,44 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     return cuda_check("k5_walk");
 }
 
-// COUNT pair walk (L >= 3): one 1024-thread CTA per SM (the K4 guided slices assume exactly that grid)
+// COUNT staged walk (L >= 3: k5_runs, or k5_pairs with FZ_COUNT_WALK=pairs): one 1024-thread CTA per SM (the K4
+// guided slices assume exactly that grid)
 template <int D, int T = 0>
-fz_status launch_pairs_d(int t, const PairPlan &pp, const WalkArgs &a, const uint64_t *C, const uint32_t *cardT,
-                         uint64_t Rcol, cudaStream_t s)
+fz_status launch_pairs_d(int t, const PairPlan &pp, const WalkArgs &a, const uint64_t *C, const uint64_t *W,
+                         const uint32_t *cardT, uint64_t Rcol, cudaStream_t s)
 {
     if constexpr (T + 3 <= D) {
-        if (t != T) return launch_pairs_d<D, T + 1>(t, pp, a, C, cardT, Rcol, s);
-        const bool pairs = count_walk_pairs();
-        auto kern = pairs ? (pp.u8 ? fzk::k5_pairs<D, T, true> : fzk::k5_pairs<D, T, false>)
-                          : (pp.u8 ? fzk::k5_runs<D, T, true> : fzk::k5_runs<D, T, false>);
-        FZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem));
-        FZ_CUDA(launch_pdl(kern, dim3((unsigned)device_sms()), dim3(fzk::kCountThreads), pp.smem, s, a.G,
-                           (uint64_t)a.n, a.hdr, C, (uint64_t)a.top, cardT, Rcol, pp.pg, pp.f0n));
+        if (t != T) return launch_pairs_d<D, T + 1>(t, pp, a, C, W, cardT, Rcol, s);
+        auto go = [&](auto kern, auto... extra) -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem);
+            if (e != cudaSuccess) return e;
+            return launch_pdl(kern, dim3((unsigned)device_sms()), dim3(fzk::kCountThreads), pp.smem, s, a.G,
+                              (uint64_t)a.n, a.hdr, C, (uint64_t)a.top, cardT, Rcol, pp.pg, pp.f0n, extra...);
+        };
+        const uint64_t *W2 = W + (uint64_t)(D - T - 2) * a.top;   // W_{L-2}: an outer prefix's lookups
+        if (count_walk_pairs())
+            FZ_CUDA(pp.u8 ? go(fzk::k5_pairs<D, T, true>) : go(fzk::k5_pairs<D, T, false>));
+        else
+            FZ_CUDA(pp.u8 ? go(fzk::k5_runs<D, T, true>, W2) : go(fzk::k5_runs<D, T, false>, W2));
         ++g_launches;
-        return cuda_check("k5_pairs");
+        return cuda_check("k5_pairs / k5_runs");
     } else {
         return fail(FZ_EINVAL, "pair walk: t=%d not instantiated for d=%d", t, D);
     }
 }
 
 template <int D = 3>
-fz_status launch_pairs(int d, int t, const PairPlan &pp, const WalkArgs &a, const uint64_t *C, const uint32_t *cardT,
-                       uint64_t Rcol, cudaStream_t s)
+fz_status launch_pairs(int d, int t, const PairPlan &pp, const WalkArgs &a, const uint64_t *C, const uint64_t *W,
+                       const uint32_t *cardT, uint64_t Rcol, cudaStream_t s)
 {
     if constexpr (D <= FZ_MAX_D) {
-        if (d == D) return launch_pairs_d<D>(t, pp, a, C, cardT, Rcol, s);
-        return launch_pairs<D + 1>(d, t, pp, a, C, cardT, Rcol, s);
+        if (d == D) return launch_pairs_d<D>(t, pp, a, C, W, cardT, Rcol, s);
+        return launch_pairs<D + 1>(d, t, pp, a, C, W, cardT, Rcol, s);
     } else {
         return fail(FZ_EINVAL, "d=%d not instantiated", d);
     }
 }
+
 
 template <int D, int T = 0>
 fz_status launch_walk_d(int t, int mode, const WalkArgs &a, cudaStream_t s)
@@ -1469,7 +1478,7 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
         return launch_deep(z.d, z.t, (int)p->mode, a, m->S, z.ltop, m->off, (cudaStream_t)stream);
     if (z.L == 0) return launch_table(z.d, (int)p->mode, a, m->off, (cudaStream_t)stream);
     if (p->mode == FZ_COUNT && p->pp.on)
-        return launch_pairs(z.d, z.t, p->pp, a, m->C, m->cardT, a.wt.R, (cudaStream_t)stream);
+        return launch_pairs(z.d, z.t, p->pp, a, m->C, m->W, m->cardT, a.wt.R, (cudaStream_t)stream);
     return launch_walk(z.d, z.t, (int)p->mode, a, (cudaStream_t)stream);
 }
 

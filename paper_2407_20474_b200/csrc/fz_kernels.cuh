@@ -1971,6 +1971,7 @@ struct PairGeo {
     // when e = 1, orbit-position steps (mod m) for the two outcomes of rmin + S3 >= g2
     uint32_t Q3, S3, cs1, cs2, is1, is2;
     uint32_t QD, RD, Fr;                // k5_runs: 32 g2 = QD m + RD; flush period (vectors) of its packed sums
+    uint64_t beta, gamma;               // the C tables' cost of a run / an outer prefix (k5_runs slice ends)
 };
 
 // x / d for any x < 2^32, d >= 1, from M = floor(2^32 / d) (d = 1: 2^32 - 1): umulhi underestimates the
@@ -2344,7 +2345,7 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
 template <int D, int T, bool U8>
 __global__ void __launch_bounds__(kCountThreads, 1)
 k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uint64_t top,
-        const uint32_t *__restrict__ cardT, uint64_t Rcol, PairGeo pg, uint32_t f0n)
+        const uint32_t *__restrict__ cardT, uint64_t Rcol, PairGeo pg, uint32_t f0n, const uint64_t *__restrict__ W2)
 {
     constexpr int L = D - T;
     static_assert(L >= 3, "run walk: at least one outer coordinate");
@@ -2360,7 +2361,7 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
     asm volatile("mov.b32 %0, %1;" : "=r"(lane) : "r"((int)(threadIdx.x & 31)));
     const uint32_t m = pg.m, g2 = G.g[L - 2];
     const uint64_t shard_begin = hdr->shard_begin, shard_len = hdr->shard_len, nslices = hdr->nslices,
-                   gw = hdr->gss_warps, fl = hdr->slice_len, total = hdr->total_units;
+                   gw = hdr->gss_warps, fl = hdr->slice_len;
     const uint32_t per = pg.mp + pg.dup;
     const uint32_t colB = pg.R16 * (U8 ? 1u : 2u);   // bytes per stored column
     uint32_t img_a;   // kept in a register (a volatile move): no per-round S2R TID / CgaCtaId re-derivation
@@ -2377,17 +2378,41 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
         const uint64_t b = shard_begin + gss_begin(si, shard_len, gw, fl),
                        e = shard_begin + gss_begin(si + 1, shard_len, gw, fl);
         if (b >= e) continue;
-        uint32_t o[NO], rj[NO + 1], oe[NO], re[NO + 1];
-        if (!pair_locate<NO>(Ct, top, G, n64, b, F0, pg, o, rj)) continue;
-        const bool to_stream_end = e >= total || !pair_locate<NO>(Ct, top, G, n64, e, F0, pg, oe, re);
-        auto at_end = [&]() -> bool {
-            if (to_stream_end) return false;
-            bool eq = true;
+        // the outer prefix holding cost rank b and its first rank ob; the slice takes the outer prefixes whose
+        // first rank lies in [b, e): it ends when the running rank ob (+ each outer prefix's cost
+        // C_{L-2}[R] = W_{L-2}[R] + beta (A + 1) + gamma, its W value prefetched when the outer prefix starts)
+        // reaches e -- no second unrank
+        uint32_t o[NO], rj[NO + 1];
+        uint64_t ob;
+        {
+            uint32_t ua[kMaxD];
 #pragma unroll
-            for (int j = 0; j < NO; ++j) eq = eq && (o[j] == oe[j]);
-            return eq;
-        };
-        if (at_end()) continue;
+            for (int j = 0; j < kMaxD; ++j) ua[j] = 0;
+            const uint64_t rin = unrank(Ct, top, G, NO, n64, b, ua, F0);
+            rj[0] = (uint32_t)n64;
+#pragma unroll
+            for (int j = 0; j < NO; ++j) {
+                o[j] = ua[j];
+                rj[j + 1] = rj[j] - o[j] * G.g[j];
+            }
+            ob = b - rin;
+            if (rin != 0) {   // o began in an earlier slice: the next outer prefix
+                const uint32_t R0 = rj[NO];
+                ob += __ldg(W2 + R0) + pg.beta * (uint64_t)(div32(R0, g2, pg.Mg2) + 1) + pg.gamma;
+                if (ob >= e) continue;
+                int i = -1;
+#pragma unroll
+                for (int j = 0; j < NO; ++j)
+                    if (o[j] > 0) i = j;
+                if (i < 0) continue;
+#pragma unroll
+                for (int j = 0; j < NO; ++j) {
+                    if (j == i) o[j] -= 1;
+                    if (j > i) o[j] = div32(rj[j], G.g[j], pg.Mg[j]);
+                    if (j >= i) rj[j + 1] = rj[j] - o[j] * G.g[j];
+                }
+            }
+        }
         uint32_t R = 0, A = 0, rmin = 0, col = 0, cb = 0, idx0 = 0;
         auto orbit = [&]() {
             const uint32_t s = col - div32(col, pg.e, pg.Me) * pg.e;
@@ -2412,7 +2437,6 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
             if (o[NO - 1] > 0) {
                 o[NO - 1] -= 1;
                 rj[NO] += G.g[NO - 1];
-                if (at_end()) return false;
                 R = rj[NO];
                 rmin += pg.S3;
                 A += pg.Q3;
@@ -2442,12 +2466,12 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
                 if (j > i) o[j] = div32(rj[j], G.g[j], pg.Mg[j]);
                 if (j >= i) rj[j + 1] = rj[j] - o[j] * G.g[j];
             }
-            if (at_end()) return false;
             load();
             return true;
         };
         load();
-        do {
+        for (;;) {
+            const uint64_t wR = __ldg(W2 + R);   // this outer prefix's lookups (used after its rounds)
             // this outer prefix: lane l takes runs k = l, l + 32, ..; run k has remainder rmin + k g2
             // (quotient q, residue rr mod m) and lies in stored column cb + orbit position idx0 + k
             const uint32_t rk = rmin + (uint32_t)lane * g2;
@@ -2522,7 +2546,9 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
                     }
                 }
             }
-        } while (advance());
+            ob += wR + pg.beta * (uint64_t)(A + 1) + pg.gamma;
+            if (ob >= e || !advance()) break;
+        }
     }
     acc = warp_sum_u64(acc);
     if (lane == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)acc);
