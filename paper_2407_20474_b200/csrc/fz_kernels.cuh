@@ -2335,11 +2335,11 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
     if (lane == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)acc);
 }
 
-// COUNT, lane-per-run variant of the same walk (k5_runs): inside an outer prefix lane l takes the runs
-// k = l, l + 32, .. <= A one after the other, stepping each run's remainder by 32 g2 without division
-// (q += QD, residue += RD); the 32 runs of a round sit in 32 consecutive stored columns (orbit order), each
-// lane reads vectors 0.. of its own column (the same index in every lane: conflict-free) and drops out
-// after its own length (divergent trip counts instead of k5_pairs' per-pass pair setup).  Same card image,
+// COUNT, lane-per-run variant of the same walk (k5_runs): every round of a warp takes the next 32 runs of the
+// outer-prefix stream, one per lane, from as many outer prefixes as that takes (no idle lanes after an outer
+// prefix's run A); the 32 runs of one outer prefix in a round sit in 32 consecutive stored columns (orbit order),
+// each lane reads vectors 0.. of its own column (the same index in every lane: conflict-free) and drops out
+// after its own length (divergent trip counts instead of k5_pairs' per-pair setup).  Same card image,
 // packed IADD3 sums (two per vector, flushed every Fr vectors), dp2a / dp4a selector tails, cost-rank
 // guided slices and slice ends as k5_pairs.
 template <int D, int T, bool U8>
@@ -2470,84 +2470,97 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
             return true;
         };
         load();
-        for (;;) {
-            const uint64_t wR = __ldg(W2 + R);   // this outer prefix's lookups (used after its rounds)
-            // this outer prefix: lane l takes runs k = l, l + 32, ..; run k has remainder rmin + k g2
-            // (quotient q, residue rr mod m) and lies in stored column cb + orbit position idx0 + k
-            const uint32_t rk = rmin + (uint32_t)lane * g2;
-            uint32_t q = div32(rk, m, pg.Mm), rr = rk - q * m;
-            uint32_t base = idx0;   // orbit position of the round's first run, mod m'
-            // the longest run of this outer prefix (run A) has (R / m + 1) / VE full vectors: one flush chunk of
-            // the packed sums suffices when that is at most Fr (uniform; always on C4)
-            const bool one_chunk = ((div32(R, m, pg.Mm) + 1) >> VSH) <= pg.Fr;
-            for (uint32_t kb = 0; kb <= A; kb += 32) {
-                const uint32_t len = (kb + lane <= A) ? q + 1 : 0u;
-                const uint32_t jp = base + lane;   // < m' + 31 with duplicates, reduced below without
-                uint32_t a = img_a + (cb + (pg.dup ? jp : jp - div32(jp, pg.mp, pg.Mmp) * pg.mp)) * colB;
-                const uint32_t N = len >> VSH;
-                uint32_t sum = 0, j = 0;
-                auto span = [&](uint32_t je) {   // vectors [j, je) of this lane's run into the packed sums
-                    uint32_t a0 = 0, a1 = 0;
-#pragma unroll 1
-                    for (; j + 4 <= je; j += 4) {
-                        const uint4 w0 = lds128(a), w1 = lds128(a + 16), w2 = lds128(a + 32), w3 = lds128(a + 48);
-                        a0 += w0.x + w0.y;
-                        a1 += w0.z + w0.w;
-                        a0 += w1.x + w1.y;
-                        a1 += w1.z + w1.w;
-                        a0 += w2.x + w2.y;
-                        a1 += w2.z + w2.w;
-                        a0 += w3.x + w3.y;
-                        a1 += w3.z + w3.w;
-                        a += 64;
-                    }
-                    // the remaining 0..3 vectors: predicated loads (no divergent 1-step loop)
-                    const uint32_t r = je - j;
-                    if (r > 0) {
-                        const uint4 w0 = lds128(a);
-                        a0 += w0.x + w0.y;
-                        a1 += w0.z + w0.w;
-                    }
-                    if (r > 1) {
-                        const uint4 w1 = lds128(a + 16);
-                        a0 += w1.x + w1.y;
-                        a1 += w1.z + w1.w;
-                    }
-                    if (r > 2) {
-                        const uint4 w2 = lds128(a + 32);
-                        a0 += w2.x + w2.y;
-                        a1 += w2.z + w2.w;
-                    }
-                    a += 16 * r;
-                    j = je;
-                    sum = unpack_add<U8>(a1, unpack_add<U8>(a0, sum));
-                };
-                if (one_chunk) {
-                    span(N);
-                } else {
-                    while (j < N) span((N - j < pg.Fr) ? N : j + pg.Fr);
+        uint64_t wR = __ldg(W2 + R);   // the current outer prefix's lookups (prefetched; used when it is done)
+        uint32_t c = 0;                // its next run
+        bool live = true;
+        while (live) {
+            // fill the 32 lanes with the next 32 runs of the stream, from as many outer prefixes as that takes
+            // (an outer prefix's last round no longer idles the lanes past its run A)
+            uint32_t mrmin = 0, mcb = 0, mbase = 0, mk0 = 0, mf = 0, maxR = 0;
+            bool mine = false;
+            uint32_t filled = 0;
+            while (filled < 32 && live) {
+                const uint32_t take = (A + 1 - c < 32 - filled) ? A + 1 - c : 32 - filled;
+                uint32_t bx = idx0 + c;   // orbit position of the group's first run, mod m' (with duplicates)
+                if (pg.dup) bx -= div32(bx, pg.mp, pg.Mmp) * pg.mp;
+                if ((uint32_t)lane >= filled && (uint32_t)lane < filled + take) {
+                    mine = true;
+                    mrmin = rmin;
+                    mcb = cb;
+                    mbase = bx;
+                    mk0 = c;
+                    mf = filled;
                 }
-                const uint32_t tl = len & (VE - 1);
-                if (tl) sum = add_prefix<U8>(lds128(a), tl, sum);
-                acc += sum;
-                // next round: k += 32
-                q += pg.QD;
-                rr += pg.RD;
-                if (rr >= m) {
-                    rr -= m;
-                    q += 1;
-                }
-                base += 32;
-                if (pg.dup) {   // base mod m' (one subtraction when m' >= 32)
-                    if (pg.mp >= 32) {
-                        if (base >= pg.mp) base -= pg.mp;
-                    } else {
-                        base -= div32(base, pg.mp, pg.Mmp) * pg.mp;
+                maxR = R > maxR ? R : maxR;
+                filled += take;
+                c += take;
+                if (c == A + 1) {   // this outer prefix is done: its cost, then the next one
+                    ob += wR + pg.beta * (uint64_t)(A + 1) + pg.gamma;
+                    live = ob < e && advance();
+                    if (live) {
+                        wR = __ldg(W2 + R);
+                        c = 0;
                     }
                 }
             }
-            ob += wR + pg.beta * (uint64_t)(A + 1) + pg.gamma;
-            if (ob >= e || !advance()) break;
+            // this lane's run: k = mk0 + (lane - mf) of its outer prefix; remainder rmin + k g2, stored column
+            // cb + orbit position base + (lane - mf)
+            uint32_t len = 0, a = img_a;
+            if (mine) {
+                const uint32_t li = (uint32_t)lane - mf;
+                len = div32(mrmin + (mk0 + li) * g2, m, pg.Mm) + 1;
+                const uint32_t jp = mbase + li;
+                a = img_a + (mcb + (pg.dup ? jp : jp - div32(jp, pg.mp, pg.Mmp) * pg.mp)) * colB;
+            }
+            // the round's longest run has at most (maxR / m + 1) / VE full vectors: one flush chunk of the packed
+            // sums suffices when that is at most Fr (uniform)
+            const bool one_chunk = ((div32(maxR, m, pg.Mm) + 1) >> VSH) <= pg.Fr;
+            const uint32_t N = len >> VSH;
+            uint32_t sum = 0, j = 0;
+            auto span = [&](uint32_t je) {   // vectors [j, je) of this lane's run into the packed sums
+                uint32_t a0 = 0, a1 = 0;
+#pragma unroll 1
+                for (; j + 4 <= je; j += 4) {
+                    const uint4 w0 = lds128(a), w1 = lds128(a + 16), w2 = lds128(a + 32), w3 = lds128(a + 48);
+                    a0 += w0.x + w0.y;
+                    a1 += w0.z + w0.w;
+                    a0 += w1.x + w1.y;
+                    a1 += w1.z + w1.w;
+                    a0 += w2.x + w2.y;
+                    a1 += w2.z + w2.w;
+                    a0 += w3.x + w3.y;
+                    a1 += w3.z + w3.w;
+                    a += 64;
+                }
+                // the remaining 0..3 vectors: predicated loads (no divergent 1-step loop)
+                const uint32_t r = je - j;
+                if (r > 0) {
+                    const uint4 w0 = lds128(a);
+                    a0 += w0.x + w0.y;
+                    a1 += w0.z + w0.w;
+                }
+                if (r > 1) {
+                    const uint4 w1 = lds128(a + 16);
+                    a0 += w1.x + w1.y;
+                    a1 += w1.z + w1.w;
+                }
+                if (r > 2) {
+                    const uint4 w2 = lds128(a + 32);
+                    a0 += w2.x + w2.y;
+                    a1 += w2.z + w2.w;
+                }
+                a += 16 * r;
+                j = je;
+                sum = unpack_add<U8>(a1, unpack_add<U8>(a0, sum));
+            };
+            if (one_chunk) {
+                span(N);
+            } else {
+                while (j < N) span((N - j < pg.Fr) ? N : j + pg.Fr);
+            }
+            const uint32_t tl = len & (VE - 1);
+            if (tl) sum = add_prefix<U8>(lds128(a), tl, sum);
+            acc += sum;
         }
     }
     acc = warp_sum_u64(acc);
