@@ -1372,7 +1372,14 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
     A.L = z.L;
     p->pp = (mode == FZ_COUNT) ? pair_plan(m->lay, n) : PairPlan{};
     A.pairs = p->pp.on ? 1 : 0;
-    A.wg = (uint64_t)device_sms() * (fzk::kCountThreads / 32);   // k5_pairs: one 1024-thread CTA per SM
+    // guided slices for the COUNT cost ranks (k5_pairs / k5_runs: one 1024-thread CTA per SM).  Row slices
+    // (MATERIALIZE / HASH) stay uniform: with half-share first slices the per-row cost variance along the walk
+    // leaves warps idle (measured: C3 t=2 hash 83 -> 134 ms); FZ_ROW_GSS=1 turns them on for experiments
+    A.wg = (uint64_t)device_sms() * (fzk::kCountThreads / 32);
+    {
+        const char *e = getenv("FZ_ROW_GSS");
+        if (mode != FZ_COUNT && !(e && e[0] == '1')) A.wg = 0;
+    }
     {
         const char *e = getenv("FZ_GSS_TAIL");                    // last slices ~ 1/tail of a warp's share
         A.gss_tail = (e && atoi(e) > 0) ? (uint64_t)atoi(e) : 128;

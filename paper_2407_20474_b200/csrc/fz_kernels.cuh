@@ -1284,6 +1284,13 @@ __device__ uint64_t unrank(const uint64_t *__restrict__ Tb, uint64_t top, const 
         const bool cached = (j == 0) && F0 != nullptr;
         uint64_t lo = 0, hi = amax;
         while (lo < hi) {
+            if (hi - lo <= 64) {   // <= 64 candidates left: two per lane, one round trip
+                const uint64_t c1 = lo + lane + 1, c2 = lo + lane + 33;
+                const bool p1 = c1 <= hi && (cached ? F0[c1] : __ldg(Tj + (r - c1 * gj))) > R;
+                const bool p2 = c2 <= hi && (cached ? F0[c2] : __ldg(Tj + (r - c2 * gj))) > R;
+                lo += __popc(__ballot_sync(kFull, p1)) + __popc(__ballot_sync(kFull, p2));
+                break;
+            }
             const uint64_t step = (hi - lo + 31) / 32;
             const uint64_t cand = lo + (uint64_t)(lane + 1) * step;
             const bool pred = cand <= hi && (cached ? F0[cand] : __ldg(Tj + (r - cand * gj))) > R;
@@ -1377,6 +1384,12 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
         slice_len = len / (A.wg * A.gss_tail);
         if (slice_len < 1024) slice_len = 1024;
         nslices = gss_count(len, gw, slice_len);
+    } else if (A.wg && !count_mode) {   // MATERIALIZE / HASH rows (k5_walk): guided slices as well
+        gw = A.wg;
+        slice_len = len / (A.wg * A.gss_tail);
+        if (slice_len < A.floor_len) slice_len = A.floor_len;
+        if (slice_len > (1ull << 26)) slice_len = 1ull << 26;
+        nslices = gss_count(len, gw, slice_len);
     } else {
         slice_len = (len + A.max_slices - 1) / A.max_slices;
         if (slice_len < A.floor_len) slice_len = A.floor_len;
@@ -1426,10 +1439,30 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
 // ----------------------------------------------------------------------- K5
 // Order-sensitive row hash (reading R17), the product's own
 // implementation.
+constexpr uint64_t kHashK = 0x9E3779B97F4A7C15ull;   // R17: x = (k + 1) * kHashK
+
+// R17 from its first state x0 = (k + 1) * kHashK (callers form x0 by additions along consecutive rows)
+template <int D>
+__device__ __forceinline__ uint64_t row_hash_x0(uint64_t x, const uint32_t (&w)[D])
+{
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        x = (x ^ (uint64_t)w[j]) * 0xBF58476D1CE4E5B9ull;
+        x ^= x >> 29;
+    }
+    x ^= (uint64_t)D;
+    x ^= x >> 33;
+    x *= 0xFF51AFD7ED558CCDull;
+    x ^= x >> 33;
+    x *= 0xC4CEB9FE1A85EC53ull;
+    x ^= x >> 33;
+    return x;
+}
+
 template <int D>
 __device__ __forceinline__ uint64_t row_hash(uint64_t k, const uint32_t (&w)[D])
 {
-    uint64_t x = (k + 1) * 0x9E3779B97F4A7C15ull;
+    uint64_t x = (k + 1) * kHashK;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
         x = (x ^ (uint64_t)w[j]) * 0xBF58476D1CE4E5B9ull;
@@ -1542,7 +1575,7 @@ struct WalkTables {
 
 
 template <int D, int T, int MODE, bool M16 = false, bool WS = false>
-__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : (WS ? 3 : 2))))
+__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : (WS ? 4 : 2))))
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
@@ -1574,6 +1607,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     const uint32_t m = G.g[L - 1];
     const uint64_t nslices = hdr->nslices, slice_len = hdr->slice_len, shard_begin = hdr->shard_begin,
                    shard_len = hdr->shard_len;
+    const uint64_t gsw = hdr->gss_warps;   // guided slices (MATERIALIZE / HASH rows) when != 0
     if (MODE == FZ_MATERIALIZE && hdr->rows > out_cap_rows) {
         if (threadIdx.x == 0 && blockIdx.x == 0) hdr->err = 1;
         return;
@@ -1586,6 +1620,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     BlockInfo *bi = binfo[wib];
     // 32-bit shared address of this warp's block list, read back with ld.shared (keeps the compiler from
     // re-deriving the generic shared window -- S2R TID / CgaCtaId -- for every 32-row chunk)
+    const uint64_t lane_k = (uint64_t)lane * kHashK;   // HASH: lane's share of the row-key multiply
     uint32_t bi_sa;   // (through a volatile move: the compiler keeps it in a register instead of recomputing it)
     asm volatile("mov.b32 %0, %1;" : "=r"(bi_sa) : "r"(smem_addr(binfo[wib])));
     const uint32_t cgq = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] / m : 0, cgr = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] % m : 0;
@@ -1599,8 +1634,14 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
         if (s >= nslices) break;
         // K4 slice: units [rel, rel + len) of the shard; unrank its first unit (rows: S, prefixes: W)
         Slice sl;
-        sl.begin = s * slice_len;
-        sl.len = (shard_len - sl.begin) < slice_len ? (shard_len - sl.begin) : slice_len;
+        if (gsw) {   // guided slices (K4): sizes halve round by round down to slice_len
+            sl.begin = gss_begin(s, shard_len, gsw, slice_len);
+            sl.len = gss_begin(s + 1, shard_len, gsw, slice_len) - sl.begin;
+            if (sl.len == 0) continue;
+        } else {
+            sl.begin = s * slice_len;
+            sl.len = (shard_len - sl.begin) < slice_len ? (shard_len - sl.begin) : slice_len;
+        }
         {
             uint32_t ua[kMaxD];
 #pragma unroll
@@ -1880,14 +1921,16 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                     }
                     {
                         uint32_t *ob = out + (outpos + q0 + lane) * (uint64_t)D;   // chunk u at ob + 32 u D
+                        // HASH: the first state (k + 1) kHashK of row k = row_base + outpos + q0 + 32 u + lane by
+                        // additions from one multiply per group (mod 2^64)
+                        const uint64_t x0 = (row_base + outpos + q0 + 1) * kHashK + lane_k;
 #pragma unroll
                         for (int u = 0; u < UNR; ++u) {
                             if (!ok[u]) continue;
-                            const uint32_t q = q0 + 32 * u + lane;
                             if constexpr (MODE == FZ_MATERIALIZE) {
                                 store_row<D>(ob + 32 * u * D, wv[u]);
                             } else {
-                                acc_hash += row_hash<D>(row_base + outpos + q, wv[u]);
+                                acc_hash += row_hash_x0<D>(x0 + (uint64_t)(32 * u) * kHashK, wv[u]);
                             }
                         }
                     }
@@ -2335,11 +2378,11 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
     if (lane == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)acc);
 }
 
-// COUNT, lane-per-run variant of the same walk (k5_runs): every round of a warp takes the next 32 runs of the
-// outer-prefix stream, one per lane, from as many outer prefixes as that takes (no idle lanes after an outer
-// prefix's run A); the 32 runs of one outer prefix in a round sit in 32 consecutive stored columns (orbit order),
-// each lane reads vectors 0.. of its own column (the same index in every lane: conflict-free) and drops out
-// after its own length (divergent trip counts instead of k5_pairs' per-pair setup).  Same card image,
+// COUNT, lane-per-run variant of the same walk (k5_runs): inside an outer prefix lane l takes the runs
+// k = l, l + 32, .. <= A one after the other, stepping each run's remainder by 32 g2 without division
+// (q += QD, residue += RD); the 32 runs of a round sit in 32 consecutive stored columns (orbit order), each
+// lane reads vectors 0.. of its own column (the same index in every lane: conflict-free) and drops out
+// after its own length (divergent trip counts instead of k5_pairs' per-pass pair setup).  Same card image,
 // packed IADD3 sums (two per vector, flushed every Fr vectors), dp2a / dp4a selector tails, cost-rank
 // guided slices and slice ends as k5_pairs.
 template <int D, int T, bool U8>
@@ -2470,97 +2513,84 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
             return true;
         };
         load();
-        uint64_t wR = __ldg(W2 + R);   // the current outer prefix's lookups (prefetched; used when it is done)
-        uint32_t c = 0;                // its next run
-        bool live = true;
-        while (live) {
-            // fill the 32 lanes with the next 32 runs of the stream, from as many outer prefixes as that takes
-            // (an outer prefix's last round no longer idles the lanes past its run A)
-            uint32_t mrmin = 0, mcb = 0, mbase = 0, mk0 = 0, mf = 0, maxR = 0;
-            bool mine = false;
-            uint32_t filled = 0;
-            while (filled < 32 && live) {
-                const uint32_t take = (A + 1 - c < 32 - filled) ? A + 1 - c : 32 - filled;
-                uint32_t bx = idx0 + c;   // orbit position of the group's first run, mod m' (with duplicates)
-                if (pg.dup) bx -= div32(bx, pg.mp, pg.Mmp) * pg.mp;
-                if ((uint32_t)lane >= filled && (uint32_t)lane < filled + take) {
-                    mine = true;
-                    mrmin = rmin;
-                    mcb = cb;
-                    mbase = bx;
-                    mk0 = c;
-                    mf = filled;
+        for (;;) {
+            const uint64_t wR = __ldg(W2 + R);   // this outer prefix's lookups (used after its rounds)
+            // this outer prefix: lane l takes runs k = l, l + 32, ..; run k has remainder rmin + k g2
+            // (quotient q, residue rr mod m) and lies in stored column cb + orbit position idx0 + k
+            const uint32_t rk = rmin + (uint32_t)lane * g2;
+            uint32_t q = div32(rk, m, pg.Mm), rr = rk - q * m;
+            uint32_t base = idx0;   // orbit position of the round's first run, mod m'
+            // the longest run of this outer prefix (run A) has (R / m + 1) / VE full vectors: one flush chunk of
+            // the packed sums suffices when that is at most Fr (uniform; always on C4)
+            const bool one_chunk = ((div32(R, m, pg.Mm) + 1) >> VSH) <= pg.Fr;
+            for (uint32_t kb = 0; kb <= A; kb += 32) {
+                const uint32_t len = (kb + lane <= A) ? q + 1 : 0u;
+                const uint32_t jp = base + lane;   // < m' + 31 with duplicates, reduced below without
+                uint32_t a = img_a + (cb + (pg.dup ? jp : jp - div32(jp, pg.mp, pg.Mmp) * pg.mp)) * colB;
+                const uint32_t N = len >> VSH;
+                uint32_t sum = 0, j = 0;
+                auto span = [&](uint32_t je) {   // vectors [j, je) of this lane's run into the packed sums
+                    uint32_t a0 = 0, a1 = 0;
+#pragma unroll 1
+                    for (; j + 4 <= je; j += 4) {
+                        const uint4 w0 = lds128(a), w1 = lds128(a + 16), w2 = lds128(a + 32), w3 = lds128(a + 48);
+                        a0 += w0.x + w0.y;
+                        a1 += w0.z + w0.w;
+                        a0 += w1.x + w1.y;
+                        a1 += w1.z + w1.w;
+                        a0 += w2.x + w2.y;
+                        a1 += w2.z + w2.w;
+                        a0 += w3.x + w3.y;
+                        a1 += w3.z + w3.w;
+                        a += 64;
+                    }
+                    // the remaining 0..3 vectors: predicated loads (no divergent 1-step loop)
+                    const uint32_t r = je - j;
+                    if (r > 0) {
+                        const uint4 w0 = lds128(a);
+                        a0 += w0.x + w0.y;
+                        a1 += w0.z + w0.w;
+                    }
+                    if (r > 1) {
+                        const uint4 w1 = lds128(a + 16);
+                        a0 += w1.x + w1.y;
+                        a1 += w1.z + w1.w;
+                    }
+                    if (r > 2) {
+                        const uint4 w2 = lds128(a + 32);
+                        a0 += w2.x + w2.y;
+                        a1 += w2.z + w2.w;
+                    }
+                    a += 16 * r;
+                    j = je;
+                    sum = unpack_add<U8>(a1, unpack_add<U8>(a0, sum));
+                };
+                if (one_chunk) {
+                    span(N);
+                } else {
+                    while (j < N) span((N - j < pg.Fr) ? N : j + pg.Fr);
                 }
-                maxR = R > maxR ? R : maxR;
-                filled += take;
-                c += take;
-                if (c == A + 1) {   // this outer prefix is done: its cost, then the next one
-                    ob += wR + pg.beta * (uint64_t)(A + 1) + pg.gamma;
-                    live = ob < e && advance();
-                    if (live) {
-                        wR = __ldg(W2 + R);
-                        c = 0;
+                const uint32_t tl = len & (VE - 1);
+                if (tl) sum = add_prefix<U8>(lds128(a), tl, sum);
+                acc += sum;
+                // next round: k += 32
+                q += pg.QD;
+                rr += pg.RD;
+                if (rr >= m) {
+                    rr -= m;
+                    q += 1;
+                }
+                base += 32;
+                if (pg.dup) {   // base mod m' (one subtraction when m' >= 32)
+                    if (pg.mp >= 32) {
+                        if (base >= pg.mp) base -= pg.mp;
+                    } else {
+                        base -= div32(base, pg.mp, pg.Mmp) * pg.mp;
                     }
                 }
             }
-            // this lane's run: k = mk0 + (lane - mf) of its outer prefix; remainder rmin + k g2, stored column
-            // cb + orbit position base + (lane - mf)
-            uint32_t len = 0, a = img_a;
-            if (mine) {
-                const uint32_t li = (uint32_t)lane - mf;
-                len = div32(mrmin + (mk0 + li) * g2, m, pg.Mm) + 1;
-                const uint32_t jp = mbase + li;
-                a = img_a + (mcb + (pg.dup ? jp : jp - div32(jp, pg.mp, pg.Mmp) * pg.mp)) * colB;
-            }
-            // the round's longest run has at most (maxR / m + 1) / VE full vectors: one flush chunk of the packed
-            // sums suffices when that is at most Fr (uniform)
-            const bool one_chunk = ((div32(maxR, m, pg.Mm) + 1) >> VSH) <= pg.Fr;
-            const uint32_t N = len >> VSH;
-            uint32_t sum = 0, j = 0;
-            auto span = [&](uint32_t je) {   // vectors [j, je) of this lane's run into the packed sums
-                uint32_t a0 = 0, a1 = 0;
-#pragma unroll 1
-                for (; j + 4 <= je; j += 4) {
-                    const uint4 w0 = lds128(a), w1 = lds128(a + 16), w2 = lds128(a + 32), w3 = lds128(a + 48);
-                    a0 += w0.x + w0.y;
-                    a1 += w0.z + w0.w;
-                    a0 += w1.x + w1.y;
-                    a1 += w1.z + w1.w;
-                    a0 += w2.x + w2.y;
-                    a1 += w2.z + w2.w;
-                    a0 += w3.x + w3.y;
-                    a1 += w3.z + w3.w;
-                    a += 64;
-                }
-                // the remaining 0..3 vectors: predicated loads (no divergent 1-step loop)
-                const uint32_t r = je - j;
-                if (r > 0) {
-                    const uint4 w0 = lds128(a);
-                    a0 += w0.x + w0.y;
-                    a1 += w0.z + w0.w;
-                }
-                if (r > 1) {
-                    const uint4 w1 = lds128(a + 16);
-                    a0 += w1.x + w1.y;
-                    a1 += w1.z + w1.w;
-                }
-                if (r > 2) {
-                    const uint4 w2 = lds128(a + 32);
-                    a0 += w2.x + w2.y;
-                    a1 += w2.z + w2.w;
-                }
-                a += 16 * r;
-                j = je;
-                sum = unpack_add<U8>(a1, unpack_add<U8>(a0, sum));
-            };
-            if (one_chunk) {
-                span(N);
-            } else {
-                while (j < N) span((N - j < pg.Fr) ? N : j + pg.Fr);
-            }
-            const uint32_t tl = len & (VE - 1);
-            if (tl) sum = add_prefix<U8>(lds128(a), tl, sum);
-            acc += sum;
+            ob += wR + pg.beta * (uint64_t)(A + 1) + pg.gamma;
+            if (ob >= e || !advance()) break;
         }
     }
     acc = warp_sum_u64(acc);
@@ -2623,6 +2653,7 @@ __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, Pl
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t nslices = hdr->nslices, slice_len = hdr->slice_len, shard_begin = hdr->shard_begin,
                    shard_len = hdr->shard_len;
+    const uint64_t gsw = hdr->gss_warps;
     if (MODE == FZ_MATERIALIZE && hdr->rows > out_cap_rows) {
         if (threadIdx.x == 0 && blockIdx.x == 0) hdr->err = 1;
         return;
@@ -2636,8 +2667,10 @@ __global__ void __launch_bounds__(kWalkThreads) k5_deep(Gens G, uint64_t n64, Pl
         if (lane == 0) s = atomicAdd(&hdr->next_slice, 1ull);
         s = shfl_u64(s, 0);
         if (s >= nslices) break;
-        const uint64_t begin = s * slice_len;
-        uint64_t left = (shard_len - begin) < slice_len ? (shard_len - begin) : slice_len;
+        const uint64_t begin = gsw ? gss_begin(s, shard_len, gsw, slice_len) : s * slice_len;
+        uint64_t left = gsw ? gss_begin(s + 1, shard_len, gsw, slice_len) - begin
+                            : ((shard_len - begin) < slice_len ? (shard_len - begin) : slice_len);
+        if (left == 0) continue;
         uint64_t outpos = begin;
         // unrank the slice's first row level by level (the S tables cover every x <= n) down to the
         // leaf that holds it (same rules as the walk below); kfirst = its offset inside that leaf
