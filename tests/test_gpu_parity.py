@@ -166,6 +166,25 @@ def test_c2_full_materialize(corc):
     assert fz.enumerate(memo, n, "count")[1] == cnt
 
 
+# ------------------------------------------- odd / non-multiple-of-4 d at 1e8 rows (word stream)
+@pytest.mark.parametrize("d,n,t", [(6, 6748, 3), (9, 1966, 5), (9, 1966, 4)], ids=lambda x: str(x))
+def test_large_materialize_odd_d(d, n, t, corc):
+    """>= 1e8-row materialize at d = 6 and d = 9 (Table 1's generators, the first n with |Z(n)| >= 1e8) element
+    by element against O2: rows leave through the 16-B word stream (d = 6 t = 3, d = 9 t = 5:
+    >= 8 rows per leading prefix) or lane by lane (d = 9 t = 4: ~9 per prefix is at the threshold)."""
+    from fzinputs import table1_gens
+
+    g = table1_gens(d)
+    want, cnt, h = corc.enumerate(n, g, use_o2=True)
+    assert cnt >= 10**8
+    memo = fz.memo_build(g, t, n + 1)
+    out, rows, _ = fz.enumerate(memo, n, "materialize")
+    assert rows == cnt
+    assert np.array_equal(_np(out).reshape(-1, d)[:rows], want.reshape(-1, d))
+    del out
+    assert fz.enumerate(memo, n, "hash")[1:] == (cnt, h)
+
+
 # ---------------------------------------------------------------------- C3
 @pytest.mark.parametrize("t", (2, 3, 4))
 def test_c3_count_hash(t, corc):
