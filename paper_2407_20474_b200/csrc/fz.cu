@@ -563,6 +563,9 @@ PairPlan pair_plan(const fz_layout *lay, uint64_t n)
     g.beta = z.beta;
     g.gamma = z.gamma;
     if (g.Fr >= 4) g.Fr &= ~3u;
+    g.bstep = 32u % mp;
+    g.bwrap = mp - g.bstep;
+    g.one_thr = ((((uint64_t)g.Fr + 1) * VE) - 1) * m;
     P.on = true;
     P.u8 = u8;
     P.f0n = f0n;

@@ -1557,7 +1557,10 @@ __device__ __forceinline__ BlockInfo lds_block_info(uint32_t a)
 }
 
 constexpr int kWalkThreads = 256;
-constexpr int kCountThreads = 1024;   // COUNT walk: one CTA per SM shares one staged card table
+#ifndef FZ_COUNT_THREADS
+#define FZ_COUNT_THREADS 1024
+#endif
+constexpr int kCountThreads = FZ_COUNT_THREADS;   // COUNT walk: one CTA per SM shares one staged card table
 template <int MODE>
 constexpr int walk_threads() { return MODE == FZ_COUNT ? kCountThreads : kWalkThreads; }
 
@@ -2014,6 +2017,8 @@ struct PairGeo {
     // when e = 1, orbit-position steps (mod m) for the two outcomes of rmin + S3 >= g2
     uint32_t Q3, S3, cs1, cs2, is1, is2;
     uint32_t QD, RD, Fr;                // k5_runs: 32 g2 = QD m + RD; flush period (vectors) of its packed sums
+    uint32_t bstep, bwrap;              // k5_runs: orbit position - 32 mod m' = p - bstep (p >= bstep) or p + bwrap
+    uint64_t one_thr;                   // k5_runs: R < one_thr <=> a run's full vectors ((R / m + 1) / VE) <= Fr
     uint64_t beta, gamma;               // the C tables' cost of a run / an outer prefix (k5_runs slice ends)
 };
 
@@ -2378,9 +2383,10 @@ k5_pairs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, ui
     if (lane == 0) atomicAdd((unsigned long long *)hdr->result, (unsigned long long)acc);
 }
 
-// COUNT, lane-per-run variant of the same walk (k5_runs): inside an outer prefix lane l takes the runs
-// k = l, l + 32, .. <= A one after the other, stepping each run's remainder by 32 g2 without division
-// (q += QD, residue += RD); the 32 runs of a round sit in 32 consecutive stored columns (orbit order), each
+// COUNT, lane-per-run variant of the same walk (k5_runs): inside an outer prefix the rounds go DOWN the
+// runs -- round r gives lane l the run k = A - 31 - 32 r + l -- so the last, partially filled round holds the
+// shortest runs; each lane steps its run's remainder by -32 g2 without division (q -= QD, residue -= RD,
+// borrow); the 32 runs of a round sit in 32 consecutive stored columns (orbit order), each
 // lane reads vectors 0.. of its own column (the same index in every lane: conflict-free) and drops out
 // after its own length (divergent trip counts instead of k5_pairs' per-pass pair setup).  Same card image,
 // packed IADD3 sums (two per vector, flushed every Fr vectors), dp2a / dp4a selector tails, cost-rank
@@ -2515,16 +2521,24 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
         load();
         for (;;) {
             const uint64_t wR = __ldg(W2 + R);   // this outer prefix's lookups (used after its rounds)
-            // this outer prefix: lane l takes runs k = l, l + 32, ..; run k has remainder rmin + k g2
-            // (quotient q, residue rr mod m) and lies in stored column cb + orbit position idx0 + k
-            const uint32_t rk = rmin + (uint32_t)lane * g2;
+            // this outer prefix, in DESCENDING rounds: round r gives lane l the run k = A - 31 - 32 r + l (run k
+            // has remainder rmin + k g2 = R - (A - k) g2: quotient q, residue rr mod m; it lies in stored column
+            // cb + orbit position idx0 + k), so the last, partially filled round holds the shortest runs.
+            // back = A - k in the first round; the lane's run exists while back <= rem (rem = A - 32 r).
+            const uint32_t back = 31u - (uint32_t)lane;
+            const uint32_t rk = (back <= A) ? R - back * g2 : 0u;
             uint32_t q = div32(rk, m, pg.Mm), rr = rk - q * m;
-            uint32_t base = idx0;   // orbit position of the round's first run, mod m'
+            // orbit position of the round's first run (k = A - 31 - 32 r) mod m': -31 = 31 (m' - 1) mod m'
+            uint32_t base;
+            {
+                const uint32_t t0 = idx0 + A + 31u * (pg.mp - 1u);
+                base = t0 - div32(t0, pg.mp, pg.Mmp) * pg.mp;
+            }
             // the longest run of this outer prefix (run A) has (R / m + 1) / VE full vectors: one flush chunk of
-            // the packed sums suffices when that is at most Fr (uniform; always on C4)
-            const bool one_chunk = ((div32(R, m, pg.Mm) + 1) >> VSH) <= pg.Fr;
-            for (uint32_t kb = 0; kb <= A; kb += 32) {
-                const uint32_t len = (kb + lane <= A) ? q + 1 : 0u;
+            // the packed sums suffices when that is at most Fr (uniform; R < one_thr)
+            const bool one_chunk = R < pg.one_thr;
+            for (int32_t rem = (int32_t)A; rem >= 0; rem -= 32) {
+                const uint32_t len = (back <= (uint32_t)rem) ? q + 1 : 0u;
                 const uint32_t jp = base + lane;   // < m' + 31 with duplicates, reduced below without
                 uint32_t a = img_a + (cb + (pg.dup ? jp : jp - div32(jp, pg.mp, pg.Mmp) * pg.mp)) * colB;
                 const uint32_t N = len >> VSH;
@@ -2573,21 +2587,11 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
                 const uint32_t tl = len & (VE - 1);
                 if (tl) sum = add_prefix<U8>(lds128(a), tl, sum);
                 acc += sum;
-                // next round: k += 32
-                q += pg.QD;
-                rr += pg.RD;
-                if (rr >= m) {
-                    rr -= m;
-                    q += 1;
-                }
-                base += 32;
-                if (pg.dup) {   // base mod m' (one subtraction when m' >= 32)
-                    if (pg.mp >= 32) {
-                        if (base >= pg.mp) base -= pg.mp;
-                    } else {
-                        base -= div32(base, pg.mp, pg.Mmp) * pg.mp;
-                    }
-                }
+                // next round: k -= 32 (32 g2 = QD m + RD)
+                const bool bw = rr < pg.RD;
+                q -= pg.QD + (bw ? 1u : 0u);
+                rr += (bw ? m : 0u) - pg.RD;
+                base = (base >= pg.bstep) ? base - pg.bstep : base + pg.bwrap;   // base - 32 mod m'
             }
             ob += wR + pg.beta * (uint64_t)(A + 1) + pg.gamma;
             if (ob >= e || !advance()) break;

@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfz.so")
+LIB_PATH = os.environ.get("FZ_LIB_PATH") or os.path.join(_HERE, "libfz.so")   # override: A/B builds (tools)
 
 MATERIALIZE, COUNT, HASH = 0, 1, 2
 _MODES = {"materialize": MATERIALIZE, "count": COUNT, "hash": HASH}
