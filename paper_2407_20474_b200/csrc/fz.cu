@@ -422,6 +422,7 @@ struct fz_plan {
     int shard, nshards;
     char *d_plan;
     PairPlan pp;
+    uint64_t rbeta = 0;   // K4 cut the slices in walk cost units (k5_walk's cost-slice instantiation)
 };
 
 // ------------------------------------------------------------ launch helpers
@@ -511,7 +512,10 @@ PairPlan pair_plan(const fz_layout *lay, uint64_t n)
     const uint64_t f0 = n / lay->g[0] + 1;
     const uint32_t f0n = (f0 <= 4096) ? (uint32_t)f0 : 0u;
     const uint64_t f0b = (uint64_t)(f0n + 1) / 2 * 16;
-    auto bytes = [&](uint64_t dd) { return f0b + (uint64_t)e * (mp + dd) * R16 * eb; };
+    // k5_runs stages the transposed image (stored columns padded to a multiple of 8), k5_pairs the column-major one
+    const bool tr = !count_walk_pairs();
+    auto ncols = [&](uint64_t dd) { const uint64_t c = (uint64_t)e * (mp + dd); return tr ? (c + 7) / 8 * 8 : c; };
+    auto bytes = [&](uint64_t dd) { return f0b + ncols(dd) * R16 * eb; };
     uint32_t dup = 31;
     if (bytes(31) > kPairSmemMax) dup = 0;
     if (bytes(dup) > kPairSmemMax) return P;
@@ -537,6 +541,8 @@ PairPlan pair_plan(const fz_layout *lay, uint64_t n)
     g.inv = inv;
     g.R16 = (uint32_t)R16;
     g.ncolv = e * (mp + dup);
+    g.ncolv8 = (uint32_t)ncols(dup);
+    g.vstride = g.ncolv8 * 16;
     // flush period (iterations of 4 cards per packed lane: a Y and an X word pair)
     // flush period of the packed accumulators (iterations; each adds 4 cards per packed lane: two Y words, two
     // X words), a multiple of 4 (the unrolled step) when at least 4
@@ -594,6 +600,10 @@ std::vector<uint64_t> host_cost_tables(const fz_layout *lay)
 }
 
 constexpr uint64_t kPlanHeader = 256;
+// cost slices of the MATERIALIZE / HASH walk (measured on Table 1 rows, C2, C3: profiles/r02_cost_slices.md)
+constexpr uint64_t kRowBeta = 16;            // walk cost of a visited leading prefix, in rows (FZ_ROW_BETA)
+constexpr uint64_t kCostSlicesPerWarp = 4;   // slices per resident warp with cost slices
+constexpr double kCostRho = 64.0;            // cost slices when n / (L g_L) < kCostRho (short rounds)
 
 // K5 queue granularity: slices per resident warp (measured optimum: 16 for MATERIALIZE / HASH, whose
 // slices are row ranges; 64 for COUNT, whose outer prefixes vary more in work)
@@ -719,6 +729,7 @@ struct WalkArgs {
     uint32_t *out;
     uint64_t cap;
     uint64_t row_base;
+    bool cs = false;             // the plan's K5 slices are walk cost units (PlanHdr::rbeta != 0)
 };
 
 template <int D, int T, int MODE>
@@ -746,8 +757,9 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
     // persistent grid: exactly the resident CTAs (the walk is a grid-stride loop over slices)
     int per_sm = 0;
     // grid sized for the largest dynamic part any n can ask (the 32 KB level-0 cache), so the residency does
-    // not depend on n; the attribute must allow that size for the occupancy query (static shared memory --
-    // the MATERIALIZE word-stream staging -- plus the dynamic part may pass 48 KB)
+    // not depend on n (measured: the residency the smaller dynamic part allows is slower on Table 1 rows); the
+    // attribute must allow that size for the occupancy query (static shared memory -- the MATERIALIZE
+    // word-stream staging -- plus the dynamic part may pass 48 KB)
     const size_t smem_q = std::max<size_t>(smem, 4096 * 8);
     auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q);
@@ -763,12 +775,19 @@ fz_status launch_walk_dtm(const WalkArgs &a, cudaStream_t s)
                           a.G, (uint64_t)a.n, a.hdr, a.Tb, (uint64_t)a.top, a.wt, a.out, (uint64_t)a.cap,
                           (uint64_t)a.row_base, f0n, c16R);
     };
+    // cost slices (a.cs) run their own instantiation, so the row-slice kernels carry none of their code
     if constexpr (MODE == FZ_HASH) {
-        if (a.wt.memo16) FZ_CUDA(go(fzk::k5_walk<D, T, MODE, true>));   // the u16 copy of the rows
-        else FZ_CUDA(go(fzk::k5_walk<D, T, MODE>));
+        if (a.wt.memo16)   // the u16 copy of the rows
+            FZ_CUDA(a.cs ? go(fzk::k5_walk<D, T, MODE, true, false, true>) : go(fzk::k5_walk<D, T, MODE, true>));
+        else
+            FZ_CUDA(a.cs ? go(fzk::k5_walk<D, T, MODE, false, false, true>) : go(fzk::k5_walk<D, T, MODE>));
     } else if constexpr (MODE == FZ_MATERIALIZE && (D % 4) != 0) {
-        if (a.wt.word_stream) FZ_CUDA(go(fzk::k5_walk<D, T, MODE, false, true>));   // the word-stream variant
-        else FZ_CUDA(go(fzk::k5_walk<D, T, MODE>));
+        if (a.wt.word_stream)   // the word-stream variant
+            FZ_CUDA(a.cs ? go(fzk::k5_walk<D, T, MODE, false, true, true>) : go(fzk::k5_walk<D, T, MODE, false, true>));
+        else
+            FZ_CUDA(a.cs ? go(fzk::k5_walk<D, T, MODE, false, false, true>) : go(fzk::k5_walk<D, T, MODE>));
+    } else if constexpr (MODE == FZ_MATERIALIZE) {
+        FZ_CUDA(a.cs ? go(fzk::k5_walk<D, T, MODE, false, false, true>) : go(fzk::k5_walk<D, T, MODE>));
     } else {
         FZ_CUDA(go(fzk::k5_walk<D, T, MODE>));
     }
@@ -1387,6 +1406,23 @@ fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, 
         const char *e = getenv("FZ_GSS_TAIL");                    // last slices ~ 1/tail of a warp's share
         A.gss_tail = (e && atoi(e) > 0) ? (uint64_t)atoi(e) : 128;
     }
+    {   // MATERIALIZE / HASH through k5_walk (full memo, L >= 1, uniform slices): when the walk's rounds are
+        // short -- rho = n / (L g_L) innermost values per outer prefix on average, below kCostRho -- the time per
+        // row varies along the walk with the round structure, and the slices are cut in walk cost units (one per
+        // row plus kRowBeta per visited leading prefix), kCostSlicesPerWarp per warp; dense walks keep row
+        // slices.  FZ_ROW_BETA (0: row slices) and FZ_SLICES_PER_WARP override.
+        const bool walk = mode != FZ_COUNT && z.L > 0 && !(z.t > 0 && n >= z.ltop) && A.wg == 0;
+        const double rho = z.L > 0 ? (double)n / ((double)z.L * m->lay->g[z.L - 1]) : 0.0;
+        const char *e = getenv("FZ_ROW_BETA");
+        const uint64_t beta = (e && *e) ? (uint64_t)atoll(e) : (rho < kCostRho ? kRowBeta : 0);
+        A.rbeta = walk ? beta : 0;
+        p->rbeta = A.rbeta;
+        if (A.rbeta) {
+            static const char *se = getenv("FZ_SLICES_PER_WARP");
+            const uint64_t per_warp = (se && atoi(se) > 0) ? (uint64_t)atoi(se) : kCostSlicesPerWarp;
+            A.max_slices = (uint64_t)device_sms() * 4 * (fzk::kWalkThreads / 32) * per_warp;
+        }
+    }
     Gens G = make_gens(m->lay->g, z.d);
     const cudaError_t le = launch_pdl(fzk::k4_plan, dim3(1), dim3(32), 0, (cudaStream_t)stream, G, A,
                                       (const uint64_t *)m->S, (const uint64_t *)m->W, (const uint64_t *)m->C,
@@ -1472,6 +1508,8 @@ fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_ca
         a.wt.gmag[j] = (g == 1) ? 0 : (~0ull / g + 1);   // ceil(2^64 / g)
     }
     a.wt.card64 = m->S + (uint64_t)z.L * z.top;
+    a.wt.Wt = m->W;
+    a.cs = p->rbeta != 0;
     {   // d not a multiple of 4: rows leave as a 16-B word stream when the warp rounds are long (measured on
         // Table 1 rows: it pays from ~8 rows per leading prefix); FZ_WORD_STREAM=0/1 forces
         const char *e = getenv("FZ_WORD_STREAM");
@@ -1715,3 +1753,13 @@ void fz_free(fz_memo *m)
 }
 
 }  // extern "C"
+
+#if FZ_SLICE_TRACE
+// diagnostic builds only: copy the per-slice trace of the last k5_walk launches ({unrank cycles, walk cycles,
+// end globaltimer / 64, SM id} per slice index) into host memory
+extern "C" int fz_debug_slice_trace(void *host, uint64_t n)
+{
+    if (n > (1u << 20)) n = 1u << 20;
+    return (int)cudaMemcpyFromSymbol(host, fzk::g_slice_trace, n * sizeof(uint4));
+}
+#endif

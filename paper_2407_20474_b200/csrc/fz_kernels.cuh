@@ -62,6 +62,8 @@ struct PlanHdr {
     unsigned long long next_slice;   // K5 work queue (slices are claimed with atomicAdd)
     uint64_t gss_warps;    // != 0: guided slices (COUNT pair walk): rounds of gss_warps slices, each round
                            // half the size of the last, down to slice_len (gss_begin); 0: uniform slices
+    uint64_t rbeta;        // != 0 (MATERIALIZE / HASH, k5_walk): slices are ranges of walk COST units -- one per
+                           // row plus rbeta per leading prefix the walk visits -- instead of rows (unrank_cost)
 };
 static_assert(sizeof(PlanHdr) <= 256, "plan header");
 
@@ -74,6 +76,7 @@ struct PlanArgs {
     int pairs;           // COUNT pair walk: units are cost ranks of the C tables, cut at outer prefixes
     uint64_t wg;         // pair walk: warps of the K5 grid (guided slice rounds)
     uint64_t gss_tail;   // pair walk: the last slices are ~ 1/gss_tail of a warp's share
+    uint64_t rbeta;      // MATERIALIZE / HASH with k5_walk: cost of a visited leading prefix in rows (0: row slices)
 };
 
 // Guided slices (pair walk): round r has `wg` slices of (len >> (r + 1)) / wg units each, until that
@@ -323,6 +326,13 @@ __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint4 lds128(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
 {
@@ -1330,6 +1340,60 @@ __device__ uint64_t row_rank(const uint64_t *__restrict__ S, uint64_t top, const
     return R;
 }
 
+// Walk cost units (MATERIALIZE / HASH slices): every leading prefix a = (a_1..a_L) the walk visits costs beta
+// units and then one unit per row of its memo block, in the walk's (descending lex) order.  The units of the
+// subtrees with coordinate j >= c are C_j[r - c g_j], C_j = S_j + beta W_j (both satisfy X_j[y] =
+// sum_a X_{j+1}[y - a g_j] for j < L), so the search is unrank's with C in place of T.  Returns the units left
+// inside the leaf a (R' < beta + card: R' < beta = inside its visit, else row R' - beta of its block) and,
+// in rows_before, the rows of Z(n) before a (the S part of the skipped subtrees).  F0: level 0 of C cached.
+__device__ __forceinline__ uint64_t unrank_cost(const uint64_t *__restrict__ S, const uint64_t *__restrict__ Wt, uint64_t beta,
+                                uint64_t top, const Gens &G, int L, uint64_t n, uint64_t R, uint32_t *a,
+                                const uint64_t *F0, uint64_t &rows_before)
+{
+    const int lane = threadIdx.x & 31;
+    uint64_t r = n, rb = 0;
+    for (int j = 0; j < L; ++j) {
+        const uint64_t *Sj = S + (uint64_t)j * top, *Wj = Wt + (uint64_t)j * top;
+        const uint64_t gj = G.g[j];
+        const uint64_t amax = r / gj;
+        const bool cached = (j == 0) && F0 != nullptr;
+        auto C = [&](uint64_t c) -> uint64_t {
+            const uint64_t x = r - c * gj;
+            return cached ? F0[c] : __ldg(Sj + x) + beta * __ldg(Wj + x);
+        };
+        uint64_t lo = 0, hi = amax;
+        while (lo < hi) {
+            if (hi - lo <= 64) {   // <= 64 candidates left: two per lane, one round trip
+                const uint64_t c1 = lo + lane + 1, c2 = lo + lane + 33;
+                const bool p1 = c1 <= hi && C(c1) > R;
+                const bool p2 = c2 <= hi && C(c2) > R;
+                lo += __popc(__ballot_sync(kFull, p1)) + __popc(__ballot_sync(kFull, p2));
+                break;
+            }
+            const uint64_t step = (hi - lo + 31) / 32;
+            const uint64_t cand = lo + (uint64_t)(lane + 1) * step;
+            const bool pred = cand <= hi && C(cand) > R;
+            const unsigned bal = __ballot_sync(kFull, pred);
+            const int m = __popc(bal);
+            const uint64_t nlo = lo + (uint64_t)m * step;
+            uint64_t nhi = lo + (uint64_t)(m + 1) * step - 1;
+            if (nhi > hi) nhi = hi;
+            lo = nlo;
+            hi = nhi;
+        }
+        a[j] = (uint32_t)lo;
+        if (lo + 1 <= amax) {   // the later subtrees (a_j > lo came first): their units and rows
+            const uint64_t x = r - (lo + 1) * gj;
+            const uint64_t fS = __ldg(Sj + x);
+            R -= cached ? F0[lo + 1] : fS + beta * __ldg(Wj + x);
+            rb += fS;
+        }
+        r -= lo * gj;
+    }
+    rows_before = rb;
+    return R;
+}
+
 // nextCandidate over the first nl coordinates: the rightmost nonzero a_i, i < nl,
 // decrements and the later ones restart at their maximum r_j / g_j; false at the end of the stream.
 __device__ __forceinline__ bool prefix_next(uint32_t *a, const Gens &G, int nl, uint64_t n)
@@ -1377,7 +1441,24 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
     const uint64_t U = __ldg(Tb + A.n);
     const uint64_t ub = mul_div(U, A.shard, A.nshards);
     const uint64_t ue = mul_div(U, A.shard + 1, A.nshards);
-    const uint64_t len = ue - ub;
+    uint64_t len = ue - ub;
+    // MATERIALIZE / HASH through k5_walk: the shard stays the row range [ub, ue); its slices cut the walk's cost
+    // units (unrank_cost) between the units of its first and last rows, cost(x) = x + rbeta (leading prefixes
+    // up to and including the one holding row x), so that sparse parts of the walk (many visited prefixes per
+    // row) get as many slices as their work asks
+    uint64_t cb = ub;
+    const bool cost_slices = !A.pairs && !count_mode && A.rbeta && A.L > 0;
+    if (cost_slices) {
+        auto cost_of = [&](uint64_t x) -> uint64_t {
+            if (x >= U) return U + A.rbeta * __ldg(W + A.n);
+            uint32_t a[kMaxD];
+            for (int j = 0; j < kMaxD; ++j) a[j] = 0;
+            unrank(S, A.top, G, A.L, A.n, x, a);
+            return x + A.rbeta * (row_rank(W, A.top, G, A.L, A.n, a) + 1);
+        };
+        cb = cost_of(ub);
+        len = cost_of(ue) - cb;
+    }
     uint64_t slice_len, nslices, gw = 0;
     if (A.pairs) {
         gw = A.wg;
@@ -1424,8 +1505,9 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
         h.result[1] = 0;
         h.err = 0;
         h.total_units = U;
-        h.shard_begin = ub;
+        h.shard_begin = cost_slices ? cb : ub;
         h.shard_len = len;
+        h.rbeta = cost_slices ? A.rbeta : 0;
         h.slice_len = slice_len;
         h.nslices = nslices;
         h.row_begin = rb;
@@ -1556,6 +1638,15 @@ __device__ __forceinline__ BlockInfo lds_block_info(uint32_t a)
     return b;
 }
 
+#ifndef FZ_SLICE_TRACE
+#define FZ_SLICE_TRACE 0   // diagnostic builds: per-slice unrank / walk cycles of k5_walk (fz_debug_slice_trace)
+#endif
+#if FZ_SLICE_TRACE
+__device__ uint4 g_slice_trace[1u << 20];
+#endif
+#ifndef FZ_WS_GROUP
+#define FZ_WS_GROUP 1   // word stream: 32-row chunks whose memo loads are in flight together (4: more registers, spills)
+#endif
 constexpr int kWalkThreads = 256;
 #ifndef FZ_COUNT_THREADS
 #define FZ_COUNT_THREADS 1024
@@ -1570,6 +1661,7 @@ struct WalkTables {
     const uint32_t *memo;    // CSR rows, t u32 each
     const uint16_t *memo16;  // the same rows as t u16 each (large memos with small coordinates), or nullptr
     const uint64_t *card64;  // card = S_L, natural layout
+    const uint64_t *Wt;      // leading-prefix count tables W_0..W_L (cost slices: unrank_cost)
     uint64_t gmag[kMaxD];    // division magic of each generator: x / g_j = umulhi64(x, gmag[j]) (+x if g_j = 1)
     uint32_t m;              // g_L (residue modulus of cardT / offT)
     uint64_t R;              // rows per residue column
@@ -1577,7 +1669,7 @@ struct WalkTables {
 };
 
 
-template <int D, int T, int MODE, bool M16 = false, bool WS = false>
+template <int D, int T, int MODE, bool M16 = false, bool WS = false, bool CS = false>
 __global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : (WS ? 4 : 2))))
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
@@ -1586,7 +1678,13 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
 {
     griddep_wait();   // PDL: the plan header (K4) and the memo tables are complete and visible
     extern __shared__ uint64_t f0s[];   // level-0 unrank column (f0n entries, 0 = not cached)
-    for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Tb + (n64 - (uint64_t)q * G.g[0]));
+    // cost slices (MATERIALIZE / HASH): the walk's units are rows plus rbeta per visited leading prefix, and the
+    // cached level-0 column holds C_0 = S_0 + rbeta W_0 (unrank_cost)
+    const uint64_t rbeta = (MODE != FZ_COUNT && CS) ? hdr->rbeta : 0;   // CS: the cost-slice instantiation
+    for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) {
+        const uint64_t x = n64 - (uint64_t)q * G.g[0];
+        f0s[q] = __ldg(Tb + x) + (rbeta ? rbeta * __ldg(wt.Wt + x) : 0);
+    }
     // COUNT, L = 2: card[x] = S_L[x], x <= n, as u16 in shared memory after f0s, residue-major w.r.t.
     // m = g_L with c16R entries per residue column (16-B aligned columns; c16R = 0: not staged)
     uint16_t *c16 = reinterpret_cast<uint16_t *>(f0s + ((f0n + 1) & ~1u));
@@ -1599,7 +1697,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     constexpr int L = D - T;
     static_assert(L >= 1, "at least one leading coordinate");
     __shared__ BlockInfo binfo[MODE == FZ_COUNT ? 1 : kWalkThreads / 32][32];   // MAT/HASH block lists
-    // MATERIALIZE with d not a multiple of 4: per-warp staging of 128 rows as a word stream (+ 3 words of phase)
+    // MATERIALIZE with d not a multiple of 4 (the WS variant): per-warp staging of 128 rows as a word stream (+ 3 words of phase)
     constexpr bool kWordStream = WS && MODE == FZ_MATERIALIZE && (D % 4) != 0;
     constexpr int kUnr = (MODE == FZ_MATERIALIZE) ? 4 : 2;   // 32-row chunks per store group (d >= 7 with 2: slower)
     __shared__ __align__(16) uint32_t wsb[kWordStream ? kWalkThreads / 32 : 1][kWordStream ? 32 * kUnr * D + 4 : 1];
@@ -1636,6 +1734,9 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
         s = shfl_u64(s, 0);
         if (s >= nslices) break;
         // K4 slice: units [rel, rel + len) of the shard; unrank its first unit (rows: S, prefixes: W)
+#if FZ_SLICE_TRACE
+        const long long tr_t0 = clock64();
+#endif
         Slice sl;
         if (gsw) {   // guided slices (K4): sizes halve round by round down to slice_len
             sl.begin = gss_begin(s, shard_len, gsw, slice_len);
@@ -1645,18 +1746,33 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
             sl.begin = s * slice_len;
             sl.len = (shard_len - sl.begin) < slice_len ? (shard_len - sl.begin) : slice_len;
         }
+        // cost slices: visit units of the slice's first leading prefix still inside the slice (rbeta, or the
+        // rest of them when the slice starts inside that visit; 0 when it starts inside its rows)
+        uint64_t vfirst = rbeta;
         {
             uint32_t ua[kMaxD];
 #pragma unroll
             for (int j = 0; j < kMaxD; ++j) ua[j] = 0;
-            const uint64_t k0 = unrank(Tb, top, G, L, n64, shard_begin + sl.begin, ua, f0n ? f0s : nullptr);
-            sl.k0 = (MODE == FZ_COUNT) ? 0 : k0;
+            if (rbeta) {
+                uint64_t rows_before;
+                const uint64_t Rp = unrank_cost(Tb, wt.Wt, rbeta, top, G, L, n64, shard_begin + sl.begin, ua,
+                                                f0n ? f0s : nullptr, rows_before);
+                sl.k0 = Rp >= rbeta ? Rp - rbeta : 0;
+                vfirst = Rp >= rbeta ? 0 : rbeta - Rp;
+                sl.begin = rows_before + sl.k0 - hdr->row_begin;   // the slice's first row, shard-relative
+            } else {
+                const uint64_t k0 = unrank(Tb, top, G, L, n64, shard_begin + sl.begin, ua, f0n ? f0s : nullptr);
+                sl.k0 = (MODE == FZ_COUNT) ? 0 : k0;
+            }
 #pragma unroll
             for (int j = 0; j < L; ++j) sl.a[j] = ua[j];
         }
         uint32_t a[L];
 #pragma unroll
         for (int j = 0; j < L; ++j) a[j] = sl.a[j];
+#if FZ_SLICE_TRACE
+        const long long tr_t1 = clock64();
+#endif
         uint32_t r_in = n;
 #pragma unroll
         for (int j = 0; j < L - 1; ++j) r_in -= a[j] * G.g[j];
@@ -1825,7 +1941,31 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 }
                 const uint32_t excl = incl - c;
                 const uint32_t total = __shfl_sync(kFull, incl, 31);
-                const uint32_t use = (uint64_t)total < left ? total : (uint32_t)left;
+                uint32_t use;   // rows of this round inside the slice
+                if (rbeta) {
+                    // cost budget: lane l (a valid prefix, l <= v) costs its visit (vfirst for lane 0, rbeta for
+                    // the others) plus its c rows; the valid lanes are 0..min(v, 31)
+                    const uint64_t nvis = (uint64_t)((uint32_t)lane < (uint32_t)v ? lane : v);
+                    const uint64_t cincl = incl + vfirst + rbeta * nvis;   // units of lanes 0..lane
+                    const uint64_t ctot = shfl_u64(cincl, 31);
+                    if (ctot <= left) {
+                        use = total;
+                        left -= ctot;
+                    } else {   // the slice ends in lane j: its rows after the budget's end belong to the next slice
+                        const unsigned over = __ballot_sync(kFull, cincl > left);
+                        const int j = __ffs(over) - 1;
+                        const uint64_t cex = shfl_u64(cincl, j) - __shfl_sync(kFull, c, j) -
+                                             (j == 0 ? vfirst : rbeta);   // units before lane j
+                        const uint64_t vis = (j == 0) ? vfirst : rbeta;
+                        const uint32_t cj = __shfl_sync(kFull, c, j), exj = __shfl_sync(kFull, excl, j);
+                        const uint64_t in_rows = left > cex + vis ? left - cex - vis : 0;   // < cj
+                        use = exj + (uint32_t)(in_rows < cj ? in_rows : cj);
+                        left = 0;
+                    }
+                    vfirst = rbeta;
+                } else {
+                    use = (uint64_t)total < left ? total : (uint32_t)left;
+                }
                 const uint32_t cc = excl >= use ? 0u : (c < use - excl ? c : use - excl);
                 const unsigned nz = __ballot_sync(kFull, cc > 0);
                 if (cc > 0) {
@@ -1855,28 +1995,39 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                         const uint64_t G0 = (outpos + q0) * (uint64_t)D;        // first word (shard-relative)
                         const uint32_t sft = (uint32_t)(((uintptr_t)(out + G0) >> 2) & 3);
                         uint32_t *sb = wsb[wib] + sft;
+                        // WSG 32-row chunks have their memo loads in flight before their rows go to shared memory
+                        constexpr int WSG = (FZ_WS_GROUP < UNR) ? FZ_WS_GROUP : UNR;
 #pragma unroll
-                        for (int u = 0; u < UNR; ++u) {
-                            const uint32_t qb = q0 + 32 * u;
-                            uint32_t bit;
-                            asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(rel - qb));
-                            const unsigned M = __reduce_or_sync(kFull, bit);
-                            const uint32_t q = qb + lane;
-                            const int e = before + __popc(M & lm_le);
-                            before += __popc(M);
-                            if (q < use) {
-                                const BlockInfo info = lds_block_info(bi_sa + 16u * (uint32_t)e);
-                                uint32_t *rw = sb + (32 * u + lane) * D;
+                        for (int u0 = 0; u0 < UNR; u0 += WSG) {
+                            uint32_t tw[WSG][T > 0 ? T : 1], vv[WSG];
+                            bool okg[WSG];
+#pragma unroll
+                            for (int g = 0; g < WSG; ++g) {
+                                const uint32_t qb = q0 + 32 * (u0 + g);
+                                uint32_t bit;
+                                asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(rel - qb));
+                                const unsigned M = __reduce_or_sync(kFull, bit);
+                                const uint32_t q = qb + lane;
+                                const int e = before + __popc(M & lm_le);
+                                before += __popc(M);
+                                okg[g] = q < use;
+                                if (okg[g]) {
+                                    const BlockInfo info = lds_block_info(bi_sa + 16u * (uint32_t)e);
+                                    vv[g] = info.v;
+                                    if constexpr (T > 0)
+                                        load_tail<T>(reinterpret_cast<const uint32_t *>(info.memo_row + (uint64_t)q * (4 * T)),
+                                                     tw[g]);
+                                }
+                            }
+#pragma unroll
+                            for (int g = 0; g < WSG; ++g) {
+                                if (!okg[g]) continue;
+                                uint32_t *rw = sb + (32 * (u0 + g) + lane) * D;
 #pragma unroll
                                 for (int j = 0; j < L - 1; ++j) rw[j] = a[j];
-                                rw[L - 1] = info.v;
-                                if constexpr (T > 0) {
-                                    uint32_t tw[T];
-                                    load_tail<T>(reinterpret_cast<const uint32_t *>(info.memo_row + (uint64_t)q * (4 * T)),
-                                                 tw);
+                                rw[L - 1] = vv[g];
 #pragma unroll
-                                    for (int j = 0; j < T; ++j) rw[L + j] = tw[j];
-                                }
+                                for (int j = 0; j < T; ++j) rw[L + j] = tw[g][j];
                             }
                         }
                         __syncwarp();
@@ -1884,9 +2035,10 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                         const uint32_t nv = (W - head) >> 2, tail0 = head + 4 * nv;
                         uint32_t *og = out + G0;
                         if ((uint32_t)lane < head) st_cs_u32(og + lane, sb[lane]);
-                        for (uint32_t v = lane; v < nv; v += 32) {
-                            const uint4 w4 = *reinterpret_cast<const uint4 *>(sb + head + 4 * v);
-                            st_cs_v4(og + head + 4 * v, w4);
+                        {   // lane l stores vectors l, l + 32, ..: pointers advance by 512 B (no per-store 64-bit index math)
+                            uint32_t sa = smem_addr(sb + head) + 16u * (uint32_t)lane;
+                            uint32_t *gp = og + head + 4 * lane;
+                            for (uint32_t v = lane; v < nv; v += 32, sa += 512, gp += 128) st_cs_v4(gp, lds128(sa));
                         }
                         if ((uint32_t)lane < W - tail0) st_cs_u32(og + tail0 + lane, sb[tail0 + lane]);
                         __syncwarp();
@@ -1941,7 +2093,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 __syncwarp();
                 acc_rows += (lane == 0) ? use : 0;
                 outpos += use;
-                left -= use;
+                if (!rbeta) left -= use;   // cost slices: the round's units were taken above
                 if (left == 0) break;
                 if (v >= 32) {
                     v -= 32;
@@ -1973,6 +2125,16 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
             colbase = (uint64_t)(r_in - q * m) * wt.R + q;
         }
         }
+#if FZ_SLICE_TRACE
+        if (lane == 0 && s < (1u << 20)) {
+            uint64_t gt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+            uint32_t smid;
+            asm("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_slice_trace[s] = make_uint4((uint32_t)(tr_t1 - tr_t0), (uint32_t)(clock64() - tr_t1), (uint32_t)(gt / 64),
+                                          smid);
+        }
+#endif
     }
     acc_rows = warp_sum_u64(acc_rows);
     if (lane == 0) atomicAdd((unsigned long long *)result, (unsigned long long)acc_rows);
@@ -2011,6 +2173,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
 struct PairGeo {
     uint32_t m, dlt, e, mp, dup, inv;   // m = g_{L-1}, Delta = g2 mod m, e = gcd(Delta, m), m' = m/e, inverse
     uint32_t R16, ncolv, F;             // entries per stored column, stored columns e (m' + dup), flush period
+    uint32_t ncolv8, vstride;           // k5_runs' transposed image: ncolv rounded up to 8, bytes between a column's vectors
     uint32_t Mm, Mg2, Me, Mmp;          // div32 magics of m, g2, e, m'
     uint32_t Mg[kMaxD];                 // div32 magics of the generators (outer carry)
     // the common outer step (a_{L-3} decrements: R += g3, g3 = Q3 g2 + S3): column steps (mod m) and,
@@ -2028,13 +2191,6 @@ __device__ __forceinline__ uint32_t div32(uint32_t x, uint32_t d, uint32_t M)
 {
     const uint32_t q = __umulhi(x, M);
     return (x - q * d >= d) ? q + 1 : q;
-}
-
-__device__ __forceinline__ uint4 lds128(uint32_t a)
-{
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
 }
 
 template <bool U8>
@@ -2103,22 +2259,35 @@ __device__ __forceinline__ bool pair_locate(const uint64_t *__restrict__ Ct, uin
 }
 
 // the card image of the COUNT walks: stored column vp = coset s, orbit position j -> residue column
-// (s + (j mod m') Delta) mod m, R16 entries each (card[col + v m] for col + v m <= n, else 0)
-template <bool U8>
+// (s + (j mod m') Delta) mod m, R16 entries each (card[col + v m] for col + v m <= n, else 0).
+// Column-major (k5_pairs): column vp is R16 consecutive entries.  Transposed (TR, k5_runs): 16-B vector vv of
+// every stored column in turn -- vector (vp, vv) at byte (vv ncolv8 + vp) 16, ncolv8 = ncolv rounded up to 8 --
+// so the vectors of any 8 consecutive stored columns lie in 8 distinct bank groups whatever their vector
+// indices (a round's tails and remainders are conflict-free, not only its common vector index).
+template <bool U8, bool TR = false>
 __device__ __forceinline__ void stage_card_image(uint8_t *img, const PairGeo &pg, const uint32_t *__restrict__ cardT,
                                                  uint64_t Rcol, uint64_t n64)
 {
     const uint32_t m = pg.m;
+    constexpr uint32_t VE = U8 ? 16 : 8;
     {
-        const uint32_t tot = pg.ncolv * pg.R16, per = pg.mp + pg.dup;
+        const uint32_t tot = (TR ? pg.ncolv8 : pg.ncolv) * pg.R16, per = pg.mp + pg.dup;
         for (uint32_t i0 = threadIdx.x; i0 < tot; i0 += 8 * blockDim.x) {
             uint32_t val[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const uint32_t i = i0 + k * blockDim.x;
                 val[k] = 0;
-                if (i < tot) {
-                    const uint32_t vp = i / pg.R16, v = i - vp * pg.R16;
+                uint32_t vp, v;
+                if constexpr (TR) {
+                    const uint32_t vv = i / (pg.ncolv8 * VE), r = i - vv * (pg.ncolv8 * VE);
+                    vp = r / VE;
+                    v = vv * VE + (r - vp * VE);
+                } else {
+                    vp = i / pg.R16;
+                    v = i - vp * pg.R16;
+                }
+                if (i < tot && vp < pg.ncolv) {
                     const uint32_t cs = vp / per, j = (vp - cs * per) % pg.mp;
                     const uint32_t col = (cs + j * pg.dlt) % m;
                     if ((uint64_t)col + (uint64_t)v * m <= n64) val[k] = __ldg(cardT + (uint64_t)col * Rcol + v);
@@ -2404,7 +2573,7 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
     extern __shared__ uint64_t f0s[];   // level-0 unrank column C_0[n - q g_0] (f0n entries), then the card image
     for (uint32_t q = threadIdx.x; q < f0n; q += blockDim.x) f0s[q] = __ldg(Ct + (n64 - (uint64_t)q * G.g[0]));
     uint8_t *img = reinterpret_cast<uint8_t *>(f0s + ((f0n + 1) & ~1u));
-    stage_card_image<U8>(img, pg, cardT, Rcol, n64);
+    stage_card_image<U8, true>(img, pg, cardT, Rcol, n64);   // transposed: conflict-free at any vector index
     __syncthreads();
     int lane;
     asm volatile("mov.b32 %0, %1;" : "=r"(lane) : "r"((int)(threadIdx.x & 31)));
@@ -2412,7 +2581,7 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
     const uint64_t shard_begin = hdr->shard_begin, shard_len = hdr->shard_len, nslices = hdr->nslices,
                    gw = hdr->gss_warps, fl = hdr->slice_len;
     const uint32_t per = pg.mp + pg.dup;
-    const uint32_t colB = pg.R16 * (U8 ? 1u : 2u);   // bytes per stored column
+    const uint32_t VS = pg.vstride;   // bytes between consecutive vectors of a stored column (transposed image)
     uint32_t img_a;   // kept in a register (a volatile move): no per-round S2R TID / CgaCtaId re-derivation
     asm volatile("mov.b32 %0, %1;" : "=r"(img_a) : "r"(smem_addr(img)));
     const uint64_t *F0 = f0n ? f0s : nullptr;
@@ -2540,14 +2709,16 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
             for (int32_t rem = (int32_t)A; rem >= 0; rem -= 32) {
                 const uint32_t len = (back <= (uint32_t)rem) ? q + 1 : 0u;
                 const uint32_t jp = base + lane;   // < m' + 31 with duplicates, reduced below without
-                uint32_t a = img_a + (cb + (pg.dup ? jp : jp - div32(jp, pg.mp, pg.Mmp) * pg.mp)) * colB;
+                uint32_t a = img_a + 16u * (cb + (pg.dup ? jp : jp - div32(jp, pg.mp, pg.Mmp) * pg.mp));
                 const uint32_t N = len >> VSH;
-                uint32_t sum = 0, j = 0;
-                auto span = [&](uint32_t je) {   // vectors [j, je) of this lane's run into the packed sums
+                uint32_t sum = 0;
+                // vectors of this lane's run up to shared byte address ae into the packed sums (the loop bound is
+                // the address itself: no separate vector counter); consecutive vectors are VS bytes apart
+                auto span = [&](uint32_t ae) {
                     uint32_t a0 = 0, a1 = 0;
 #pragma unroll 1
-                    for (; j + 4 <= je; j += 4) {
-                        const uint4 w0 = lds128(a), w1 = lds128(a + 16), w2 = lds128(a + 32), w3 = lds128(a + 48);
+                    for (; a + 3 * VS < ae; a += 4 * VS) {
+                        const uint4 w0 = lds128(a), w1 = lds128(a + VS), w2 = lds128(a + 2 * VS), w3 = lds128(a + 3 * VS);
                         a0 += w0.x + w0.y;
                         a1 += w0.z + w0.w;
                         a0 += w1.x + w1.y;
@@ -2556,33 +2727,31 @@ k5_runs(Gens G, uint64_t n64, PlanHdr *hdr, const uint64_t *__restrict__ Ct, uin
                         a1 += w2.z + w2.w;
                         a0 += w3.x + w3.y;
                         a1 += w3.z + w3.w;
-                        a += 64;
                     }
                     // the remaining 0..3 vectors: predicated loads (no divergent 1-step loop)
-                    const uint32_t r = je - j;
-                    if (r > 0) {
+                    if (a < ae) {
                         const uint4 w0 = lds128(a);
                         a0 += w0.x + w0.y;
                         a1 += w0.z + w0.w;
                     }
-                    if (r > 1) {
-                        const uint4 w1 = lds128(a + 16);
+                    if (a + VS < ae) {
+                        const uint4 w1 = lds128(a + VS);
                         a0 += w1.x + w1.y;
                         a1 += w1.z + w1.w;
                     }
-                    if (r > 2) {
-                        const uint4 w2 = lds128(a + 32);
+                    if (a + 2 * VS < ae) {
+                        const uint4 w2 = lds128(a + 2 * VS);
                         a0 += w2.x + w2.y;
                         a1 += w2.z + w2.w;
                     }
-                    a += 16 * r;
-                    j = je;
+                    a = ae;
                     sum = unpack_add<U8>(a1, unpack_add<U8>(a0, sum));
                 };
+                const uint32_t aN = a + VS * N;   // the run's partial last vector
                 if (one_chunk) {
-                    span(N);
+                    span(aN);
                 } else {
-                    while (j < N) span((N - j < pg.Fr) ? N : j + pg.Fr);
+                    while (a < aN) span((aN - a < VS * pg.Fr) ? aN : a + VS * pg.Fr);
                 }
                 const uint32_t tl = len & (VE - 1);
                 if (tl) sum = add_prefix<U8>(lds128(a), tl, sum);
