@@ -3,4 +3,4 @@
 N=$1; shift
 mkdir -p ab
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
-  --split-compile=0 -diag-suppress 128 "$@" -o ab/libfz_$N.so paper_2407_20474_b200/csrc/fz.cu
+  --split-compile=0 -diag-suppress 128,186 "$@" -o ab/libfz_$N.so paper_2407_20474_b200/csrc/fz.cu

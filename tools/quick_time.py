@@ -24,6 +24,8 @@ CFG = {
     "T63": ((13, 37, 38, 40, 41, 42), 5000, 3, "materialize"),
     "T31": ((13, 37, 38), 300000, 1, "materialize"),
     "T74": ((13, 37, 38, 40, 41, 42, 43), 2000, 4, "materialize"),
+    "T84b": ((13, 37, 38, 40, 41, 42, 43, 44), 1500, 4, "materialize"),
+    "T64": ((13, 37, 38, 40, 41, 42), 3000, 4, "materialize"),
 }
 # partial memo (f2): memo rows only for x < frac * n
 for _f in (10, 25, 50, 75, 90):
