@@ -174,8 +174,8 @@ struct Sizing {
     Layout lay{};
 };
 
-constexpr uint64_t kCountRunCost = 96;     // COUNT cost model (card lookups; measured, tools/count_tune.py): per innermost run
-constexpr uint64_t kCountOuterCost = 3072;  // ... and per outer prefix
+constexpr uint64_t kCountRunCost = 48;     // COUNT cost model (card lookups, u16 image; x2 for u8; measured, tools/count_tune.py,
+constexpr uint64_t kCountOuterCost = 1536;  // profiles/r02_shard_balance.md): per innermost run and per outer prefix
 constexpr uint64_t kWordStreamRowsPerPrefix = 8;    // MATERIALIZE word stream from this many rows per prefix
 constexpr uint64_t kRows16MinBytes = 64ull << 20;   // u16 row copy: u32 rows above this (half the 126 MB L2)
 constexpr uint64_t kRows16MaxBytes = 96ull << 20;   //   ... and the copy below this
@@ -202,13 +202,6 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
     z.t = t;
     z.L = d - t;
     z.top = top;
-    {   // cost model of the COUNT pair-walk cut (in card lookups): FZ_COUNT_RUN_COST per innermost run,
-        // FZ_COUNT_OUTER_COST per outer prefix, beyond the lookups
-        const char *e = getenv("FZ_COUNT_RUN_COST");
-        z.beta = (e && *e) ? (uint64_t)strtoull(e, nullptr, 10) : kCountRunCost;
-        const char *e2 = getenv("FZ_COUNT_OUTER_COST");
-        z.gamma = (e2 && *e2) ? (uint64_t)strtoull(e2, nullptr, 10) : kCountOuterCost;
-    }
     const int L = z.L;
     const uint64_t *card = H.S.data() + (size_t)L * top;
     const uint64_t g_cap = g_memo_cap.load();   // one snapshot of the process-wide cap per layout
@@ -225,6 +218,15 @@ fz_status size_memo(const uint32_t *g, int d, int t, uint64_t top, uint64_t memo
     }
     z.ltop = memo_top;
     for (uint64_t x = 0; x < top; ++x) z.card_max_all = std::max(z.card_max_all, card[x]);
+    {   // cost model of the COUNT walk's cut (in card lookups): FZ_COUNT_RUN_COST per innermost run,
+        // FZ_COUNT_OUTER_COST per outer prefix, beyond the lookups; a u8 card image (every card < 64) reads
+        // twice the lookups per vector, so its runs and outer prefixes weigh twice as many lookups
+        const bool u8 = z.card_max_all <= 63;
+        const char *e = getenv("FZ_COUNT_RUN_COST");
+        z.beta = (e && *e) ? (uint64_t)strtoull(e, nullptr, 10) : (u8 ? 2 : 1) * kCountRunCost;
+        const char *e2 = getenv("FZ_COUNT_OUTER_COST");
+        z.gamma = (e2 && *e2) ? (uint64_t)strtoull(e2, nullptr, 10) : (u8 ? 2 : 1) * kCountOuterCost;
+    }
     const uint64_t ltop = memo_top;
     uint64_t entries = 0, mx = 0;
     for (uint64_t x = 0; x < ltop; ++x) {

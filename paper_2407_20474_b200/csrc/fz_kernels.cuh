@@ -1523,20 +1523,36 @@ __global__ void __launch_bounds__(32) k4_plan(Gens G, PlanArgs A, const uint64_t
 // implementation.
 constexpr uint64_t kHashK = 0x9E3779B97F4A7C15ull;   // R17: x = (k + 1) * kHashK
 
+// x * M mod 2^64 for a constant M in three 32-bit multiply-adds (lo(x) lo(M) wide, then lo(x) hi(M) and
+// hi(x) lo(M) into the high word); the compiler's own 64-bit multiply takes four instructions
+__device__ __forceinline__ uint64_t mul64c(uint64_t x, uint64_t M)
+{
+    uint32_t lo, hi;
+    asm("{\n\t.reg .u32 xl, xh;\n\t.reg .u64 w;\n\t"
+        "mov.b64 {xl, xh}, %2;\n\t"
+        "mul.wide.u32 w, xl, %3;\n\t"
+        "mov.b64 {%0, %1}, w;\n\t"
+        "mad.lo.u32 %1, xl, %4, %1;\n\t"
+        "mad.lo.u32 %1, xh, %3, %1;\n\t}"
+        : "=r"(lo), "=r"(hi)
+        : "l"(x), "r"((uint32_t)M), "r"((uint32_t)(M >> 32)));
+    return ((uint64_t)hi << 32) | lo;
+}
+
 // R17 from its first state x0 = (k + 1) * kHashK (callers form x0 by additions along consecutive rows)
 template <int D>
 __device__ __forceinline__ uint64_t row_hash_x0(uint64_t x, const uint32_t (&w)[D])
 {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        x = (x ^ (uint64_t)w[j]) * 0xBF58476D1CE4E5B9ull;
+        x = mul64c(x ^ (uint64_t)w[j], 0xBF58476D1CE4E5B9ull);
         x ^= x >> 29;
     }
     x ^= (uint64_t)D;
     x ^= x >> 33;
-    x *= 0xFF51AFD7ED558CCDull;
+    x = mul64c(x, 0xFF51AFD7ED558CCDull);
     x ^= x >> 33;
-    x *= 0xC4CEB9FE1A85EC53ull;
+    x = mul64c(x, 0xC4CEB9FE1A85EC53ull);
     x ^= x >> 33;
     return x;
 }
@@ -1544,19 +1560,7 @@ __device__ __forceinline__ uint64_t row_hash_x0(uint64_t x, const uint32_t (&w)[
 template <int D>
 __device__ __forceinline__ uint64_t row_hash(uint64_t k, const uint32_t (&w)[D])
 {
-    uint64_t x = (k + 1) * kHashK;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        x = (x ^ (uint64_t)w[j]) * 0xBF58476D1CE4E5B9ull;
-        x ^= x >> 29;
-    }
-    x ^= (uint64_t)D;
-    x ^= x >> 33;
-    x *= 0xFF51AFD7ED558CCDull;
-    x ^= x >> 33;
-    x *= 0xC4CEB9FE1A85EC53ull;
-    x ^= x >> 33;
-    return x;
+    return row_hash_x0<D>((k + 1) * kHashK, w);
 }
 
 // Memo-row loads and output stores as volatile PTX: they keep program order, so a warp issues the
@@ -2270,6 +2274,39 @@ __device__ __forceinline__ void stage_card_image(uint8_t *img, const PairGeo &pg
 {
     const uint32_t m = pg.m;
     constexpr uint32_t VE = U8 ? 16 : 8;
+    if constexpr (TR) {   // one 16-B vector (VE entries of one stored column) per thread and step
+        const uint32_t nvec = pg.ncolv8 * (pg.R16 / VE), per = pg.mp + pg.dup;
+        for (uint32_t w = threadIdx.x; w < nvec; w += blockDim.x) {
+            const uint32_t vv = w / pg.ncolv8, vp = w - vv * pg.ncolv8;
+            uint32_t e[VE];
+#pragma unroll
+            for (int k = 0; k < (int)VE; ++k) e[k] = 0;
+            if (vp < pg.ncolv) {
+                const uint32_t cs = vp / per, j = (vp - cs * per) % pg.mp;
+                const uint32_t col = (cs + j * pg.dlt) % m;
+                const uint32_t *src = cardT + (uint64_t)col * Rcol;
+#pragma unroll
+                for (int k = 0; k < (int)VE; ++k) {
+                    const uint32_t v = vv * VE + k;
+                    if ((uint64_t)col + (uint64_t)v * m <= n64) e[k] = __ldg(src + v);
+                }
+            }
+            uint4 pk;
+            if constexpr (U8) {
+                pk.x = e[0] | (e[1] << 8) | (e[2] << 16) | (e[3] << 24);
+                pk.y = e[4] | (e[5] << 8) | (e[6] << 16) | (e[7] << 24);
+                pk.z = e[8 % VE] | (e[9 % VE] << 8) | (e[10 % VE] << 16) | (e[11 % VE] << 24);
+                pk.w = e[12 % VE] | (e[13 % VE] << 8) | (e[14 % VE] << 16) | (e[15 % VE] << 24);
+            } else {
+                pk.x = e[0] | (e[1] << 16);
+                pk.y = e[2] | (e[3] << 16);
+                pk.z = e[4] | (e[5] << 16);
+                pk.w = e[6] | (e[7] << 16);
+            }
+            reinterpret_cast<uint4 *>(img)[w] = pk;
+        }
+        return;
+    }
     {
         const uint32_t tot = (TR ? pg.ncolv8 : pg.ncolv) * pg.R16, per = pg.mp + pg.dup;
         for (uint32_t i0 = threadIdx.x; i0 < tot; i0 += 8 * blockDim.x) {

@@ -458,3 +458,40 @@ def test_partial_table1(d, md, n, corc):
     cnt, h = corc.count_hash(n, g, use_o2=True)
     assert fz.enumerate(memo, n, "hash")[1:] == (cnt, h)
     assert fz.enumerate(memo, n, "count")[1] == cnt
+
+
+# ------------------------------------------------ slice kinds (row slices / walk-cost slices)
+@pytest.mark.parametrize("beta,spw", [("0", "16"), ("1", "4"), ("16", "1"), ("16", "64"), ("200", "4")],
+                         ids=lambda x: str(x))
+@pytest.mark.parametrize("case", ["C2", "T95", "T1mid", "C3t3"])
+def test_slice_kinds(case, beta, spw, corc, monkeypatch):
+    """Both K5 slice kinds forced on workloads whose default is the other one: row slices (FZ_ROW_BETA=0) on
+    short-round Table 1 walks, cost slices (beta 1..200 rows per visited prefix, 1..64 slices per warp) on C2 and
+    C3: the same rows (element by element on a mid-size Table 1 walk), count and hash."""
+    from fzinputs import table1_gens
+
+    monkeypatch.setenv("FZ_ROW_BETA", beta)
+    monkeypatch.setenv("FZ_SLICES_PER_WARP", spw)
+    if case == "C2":
+        g, n, t, kat = C2.gens, C2.n, C2.t, 0x5FC4E1F53888C565
+    elif case == "C3t3":
+        g, n, t, kat = C3_GENS, C3_N, 3, 0xBE3AEBC0385B7792
+    elif case == "T95":
+        g, n, t, kat = table1_gens(9), 1500, 5, None
+    else:
+        g, n, t, kat = table1_gens(8), 1200, 4, None
+    memo = fz.memo_build(g, t, n + 1)
+    _, rows, h = fz.enumerate(memo, n, "hash")
+    if kat is None:
+        cnt, kat = corc.count_hash(n, g, use_o2=True)
+    else:
+        cnt = corc.gf_count(n, g)
+    assert (rows, h) == (cnt, kat)
+    if case in ("T1mid", "T95"):
+        out, rows, _ = fz.enumerate(memo, n, "materialize")
+        got = _np(out).reshape(-1, len(g))[:rows]
+        if case == "T1mid":
+            want, _, _ = corc.enumerate(n, g, use_o2=True)
+            assert np.array_equal(got, want)
+        else:
+            assert corc.hash_rows(got) == kat

@@ -16,6 +16,7 @@ def shard_ms(memo, n, k, s, pws, reps=3):
     best = None
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)   # the host's plan / launch calls are enqueued behind ~1 ms of GPU work
         e0.record()
         p = fz.Plan(memo, n, "count", s, k, workspace=pws)
         p.launch()

@@ -1,6 +1,8 @@
 """Strong-scaling balance of the sharded COUNT walk on one GPU: C4 (t = 3) cut into k shards, each shard's
 whole step (plan + walk) timed alone with CUDA events; reports max / mean shard time and the efficiency
-T_1 / (k * max shard) that k GPUs could reach before collective and launch costs."""
+T_1 / (k * max shard) that k GPUs could reach before collective and launch costs.  Each
+measurement starts behind ~1 ms of GPU sleep, so the host's plan creation and kernel submission overlap device
+work (as in bench.py, which enqueues its steps ahead) and the events time the device work alone."""
 import os
 import sys
 
@@ -21,7 +23,8 @@ def shard_times(g, n, t, mode, k, reps=3):
         best = None
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+            torch.cuda._sleep(2_000_000)   # ~1 ms of GPU work first: the host's plan creation and launch
+            e0.record()                    # calls are enqueued behind it and stay off the device time
             p = fz.Plan(memo, n, mode, s, k, workspace=pws)
             p.launch()
             e1.record()
