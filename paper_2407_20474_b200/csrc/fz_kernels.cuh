@@ -1648,6 +1648,12 @@ __device__ __forceinline__ BlockInfo lds_block_info(uint32_t a)
 #if FZ_SLICE_TRACE
 __device__ uint4 g_slice_trace[1u << 20];
 #endif
+#ifndef FZ_HASH_MINB
+#define FZ_HASH_MINB 4  // HASH walk, d <= 6: resident CTAs per SM the register budget is sized for
+#endif
+#ifndef FZ_HASH_UNR
+#define FZ_HASH_UNR 2   // HASH / COUNT (L <= 2) walk: 32-row chunks in flight per warp
+#endif
 #ifndef FZ_WS_GROUP
 #define FZ_WS_GROUP 1   // word stream: 32-row chunks whose memo loads are in flight together (4: more registers, spills)
 #endif
@@ -1674,7 +1680,7 @@ struct WalkTables {
 
 
 template <int D, int T, int MODE, bool M16 = false, bool WS = false, bool CS = false>
-__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (D <= 6 ? 4 : (WS ? 4 : 2))))
+__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (MODE == FZ_HASH && D <= 6 ? FZ_HASH_MINB : (D <= 6 ? 4 : (WS ? 4 : 2)))))
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
@@ -1703,7 +1709,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     __shared__ BlockInfo binfo[MODE == FZ_COUNT ? 1 : kWalkThreads / 32][32];   // MAT/HASH block lists
     // MATERIALIZE with d not a multiple of 4 (the WS variant): per-warp staging of 128 rows as a word stream (+ 3 words of phase)
     constexpr bool kWordStream = WS && MODE == FZ_MATERIALIZE && (D % 4) != 0;
-    constexpr int kUnr = (MODE == FZ_MATERIALIZE) ? 4 : 2;   // 32-row chunks per store group (d >= 7 with 2: slower)
+    constexpr int kUnr = (MODE == FZ_MATERIALIZE) ? 4 : FZ_HASH_UNR;   // 32-row chunks per group (MAT d >= 7 with 2: slower)
     __shared__ __align__(16) uint32_t wsb[kWordStream ? kWalkThreads / 32 : 1][kWordStream ? 32 * kUnr * D + 4 : 1];
     const int lane = threadIdx.x & 31, wib = (MODE == FZ_COUNT) ? 0 : threadIdx.x >> 5;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
