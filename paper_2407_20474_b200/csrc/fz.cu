@@ -19,6 +19,7 @@
 
 #include "../../include/fz.h"
 #include "fz_kernels.cuh"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges per C-ABI phase (free without an attached tool)
 
 using fzk::Gens;
 using fzk::PlanArgs;
@@ -429,6 +430,15 @@ struct fz_plan {
 
 // ------------------------------------------------------------ launch helpers
 namespace {
+
+// NVTX range over one C-ABI call (memo build, count, plan, enumerate, run_host): the phases of a step on the
+// profiler's host timeline (SURVEY §5 tracing)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 Gens make_gens(const uint32_t *g, int d)
 {
@@ -1122,6 +1132,7 @@ fz_status fz_memo_workspace_bytes(const uint32_t *gens, int d, int t, uint64_t t
 
 fz_status fz_memo_build_layout(const fz_layout *lay, void *d_ws, uint64_t ws_bytes, void *stream, fz_memo **out)
 {
+    NvtxRange nvtx("fz_memo_build");
     static const bool fuse_env = [] {
         const char *e = getenv("FZ_FUSE_MEMO");
         return !(e && e[0] == '0');
@@ -1253,6 +1264,7 @@ fz_status fz_memo_device_views(const fz_memo *m, const uint32_t **rows, const ui
 
 fz_status fz_count(const fz_memo *m, uint64_t n, void *stream, uint64_t *count)
 {
+    NvtxRange nvtx("fz_count");
     if (!m || !count) return fail(FZ_EINVAL, "NULL argument");
     if (n >= m->lay->z.top)
         return fail(FZ_EINVAL, "n=%llu >= top=%llu", (unsigned long long)n, (unsigned long long)m->lay->z.top);
@@ -1359,6 +1371,7 @@ fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t *bytes)
 fz_status fz_plan_create(const fz_memo *m, uint64_t n, fz_mode mode, int shard, int nshards, void *d_plan,
                          uint64_t plan_ws_bytes, void *stream, fz_plan **out)
 {
+    NvtxRange nvtx("fz_plan_create");
     if (!out) return fail(FZ_EINVAL, "out is NULL");
     *out = nullptr;
     if (!m) return fail(FZ_EINVAL, "NULL memo");
@@ -1484,6 +1497,7 @@ fz_status fz_plan_shard(const fz_plan *p, void *stream, uint64_t *row_begin, uin
 fz_status fz_enumerate_launch(const fz_plan *p, uint32_t *d_out, uint64_t out_capacity_rows, uint64_t row_base,
                               void *stream)
 {
+    NvtxRange nvtx("fz_enumerate_launch");
     if (!p) return fail(FZ_EINVAL, "NULL plan");
     const fz_memo *m = p->m;
     const Sizing &z = m->lay->z;
@@ -1670,6 +1684,7 @@ fz_status fz_run_host(const uint32_t *gens, int d, int t, uint64_t n, fz_mode mo
                       uint32_t *h_out, uint64_t h_out_capacity_rows, void *stream, uint64_t *rows_out,
                       uint64_t *hash_out)
 {
+    NvtxRange nvtx("fz_run_host");
     if (mode != FZ_MATERIALIZE && mode != FZ_COUNT && mode != FZ_HASH) return fail(FZ_EINVAL, "bad mode");
     if (!d_ws || ((uintptr_t)d_ws & 255)) return fail(FZ_EINVAL, "workspace NULL or not 256-byte aligned");
     const fz_layout *lay = nullptr;

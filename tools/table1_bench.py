@@ -4,7 +4,7 @@ For every row (d, memo_dim, n), gens (13,37,38[,40..45])[:d], full memo top = n+
 memo_us = fz_memo_build (K1 + K3) from a prebuilt layout, enum_us = plan + enumerate (materialize),
 both CUDA-event medians of 5 runs after 2 warm-ups, beside the paper's cpu/gpu memo us and runtime ms
 (RTX 3080 + Ryzen 3900X; context only).  Also runs the recommended t (fz_recommend_t).
-Writes a markdown table to stdout."""
+Writes a markdown table to stdout (`--csv`: the paper's Table 1 record, as CSV)."""
 import os
 import sys
 
@@ -55,7 +55,31 @@ def run(d, t, n):
     return rows, memo_us, enum_us
 
 
+def main_csv():
+    """--csv: the paper's Table 1 record (SPEC header dim,memo_dim,element,num_results,cpu_memo_us,
+    par_memo_us,runtime_ms) with this build's GPU memo build as par_memo_us and memo + enumerate as runtime_ms;
+    cpu_memo_us is the single-thread CPU memo (Alg 2) recorded by `bench.py --study f4` (profiles/r02_f4_study.jsonl;
+    blank when absent); the GPU enumerate time and factorizations/s are appended."""
+    import json
+    cpu = {}   # recorded single-thread CPU memo times (bench.py --study f4, profiles/r02_f4_study.jsonl)
+    study = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02_f4_study.jsonl")
+    if os.path.exists(study):
+        for line in open(study):
+            r = json.loads(line)
+            if "cpu_memo_us" in r and "t_paper" in r:
+                cpu[(len(r["gens"]), r["t_paper"], r["n"])] = r["cpu_memo_us"]
+    print("dim,memo_dim,element,num_results,cpu_memo_us,par_memo_us,runtime_ms,gpu_enum_us,fact_per_s")
+    for d, t, n in TABLE1_ROWS:
+        rows, mu, eu = run(d, t, n)
+        tot = (mu + eu) / 1e3
+        c = cpu.get((d, t, n))
+        print(f"{d},{t},{n},{rows},{'' if c is None else f'{c:.1f}'},{mu:.1f},{tot:.4f},{eu:.1f},"
+              f"{rows / tot * 1e3:.4e}", flush=True)
+
+
 def main():
+    if "--csv" in sys.argv:
+        return main_csv()
     print("| d | t | n | rows | memo us | enum us | total ms | fact/s | t* | t* total ms | paper gpu_memo us | paper runtime ms | paper fact/s |")
     print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for d, t, n in TABLE1_ROWS:
