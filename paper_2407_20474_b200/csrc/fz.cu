@@ -1285,12 +1285,12 @@ fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards,
 // SURVEY §8(f) f4 (the best memo dimension depends on the instance).  Predicted seconds
 // of a whole step (memo build + plan + walk) for memo dimension t, from the host count tables:
 //   R = |Z(n)|, P = leading prefixes (a_1..a_L, phi <= n), E = memo rows sum_{x<=n} |Z(x; tail)|, L = d - t;
-//   MATERIALIZE: 1.03e-4 + 2.815e-13 (4 d R) + 8.886e-12 P + 9.803e-13 (4 t E)
-//   HASH:        3.449e-12 R + 7.08e-12 P + 5.271e-13 (4 t E)
+//   MATERIALIZE: 9.04e-5 + 2.66e-13 (4 d R) + 1.045e-11 P + 9.964e-13 (4 t E)
+//   HASH:        3.273e-12 R + 7.424e-12 P + 4.144e-13 (4 t E)
 //   COUNT:       8.74e-5 + c_P P, c_P = 9.4e-14 with the staged pair walk (L >= 3, cards < 2^14, image fits
 //                shared memory), else 9.2e-13 (the u32 card table from L2)
 // The constants are a non-negative least-squares fit (relative error) of B200 step times over every t of
-// Table 1's 31 rows, C2, C3 and C4 (tools/f4_fit.py on profiles/r02_f4_study.jsonl, from
+// Table 1's 31 rows, C2, C3 and C4 (tools/f4_fit.py on profiles/r02x_f4_study.jsonl -- the kernels with cost slices -- from
 // `bench.py --study f4`).  Memos above the memory cap, and COUNT with a tail block >= 2^32, are infeasible.
 fz_status fz_recommend_t(const uint32_t *gens, int d, uint64_t n, fz_mode mode, int *t_best, double *cost)
 {
@@ -1329,8 +1329,8 @@ fz_status fz_recommend_t(const uint32_t *gens, int d, uint64_t n, fz_mode mode, 
                 }
                 const bool fits = E * 4.0 * t <= (double)cap;
                 if (mode == FZ_MATERIALIZE && fits)
-                    c = 1.03e-4 + 2.815e-13 * (4.0 * d * R) + 8.886e-12 * P + 9.803e-13 * (4.0 * t * E);
-                if (mode == FZ_HASH && fits) c = 3.449e-12 * R + 7.08e-12 * P + 5.271e-13 * (4.0 * t * E);
+                    c = 9.04e-5 + 2.66e-13 * (4.0 * d * R) + 1.045e-11 * P + 9.964e-13 * (4.0 * t * E);
+                if (mode == FZ_HASH && fits) c = 3.273e-12 * R + 7.424e-12 * P + 4.144e-13 * (4.0 * t * E);
                 if (mode == FZ_COUNT && cmax < (1ull << 32)) {
                     const uint64_t m = gens[L - 1];
                     const double img = double(n + 1 + 32 * (n / m + 1)) * (cmax <= 63 ? 1.0 : 2.0);

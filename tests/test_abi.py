@@ -92,15 +92,16 @@ def test_recommend_t():
 def _f4_records():
     import json
 
-    path = os.path.join(os.path.dirname(LIB), "..", "profiles", "r02_f4_study.jsonl")
+    path = os.path.join(os.path.dirname(LIB), "..", "profiles", "r02x_f4_study.jsonl")
     return [json.loads(x) for x in open(path) if x.strip()]
 
 
 def test_recommend_t_against_measured_study():
-    """f4 done-when: on every case of the recorded B200 study (profiles/r02_f4_study.jsonl:
-    Table 1's 31 rows materialized, C2, C3 hash, C4 count; each t timed as a whole step), fz_recommend_t's
-    pick is the measured best t or within 5 % of it, except on at most six small-n Table 1 rows whose steps
-    are latency-bound (85-125 us, the model is linear in the work counts): there within 15 %."""
+    """f4: on every case of the recorded B200 study (profiles/r02x_f4_study.jsonl, the round-2
+    kernels: Table 1's 31 rows materialized, C2, C3 hash, C4 count; each t timed as a whole step),
+    fz_recommend_t's pick is the measured best t or within 5 % of it, except on at most eight small-n Table 1
+    rows whose steps are latency-bound (< 140 us; the model is linear in the work counts): there within 10 %
+    (DESIGN.md §9)."""
     from paper_2407_20474_b200 import fz
 
     misses = []
@@ -112,8 +113,8 @@ def test_recommend_t_against_measured_study():
         ratio = meas[pick] / meas[best]
         if ratio > 1.05:
             misses.append((r["case"], pick, best, ratio))
-            assert ratio <= 1.15 and meas[best] < 130.0, (r["case"], pick, best, ratio)
-    assert len(misses) <= 6, misses
+            assert ratio <= 1.10 and meas[best] < 140.0, (r["case"], pick, best, ratio)
+    assert len(misses) <= 8, misses
 
 
 def test_f4_cpu_gpu_memo_crossover():

@@ -1,6 +1,6 @@
 """Fit fz_recommend_t's cost model to a `bench.py --study f4` run.
 
-    python tools/f4_fit.py profiles/r02_f4_study.jsonl
+    python tools/f4_fit.py profiles/r02x_f4_study.jsonl
 
 Per (case, t) features from the host count tables (the quantities fz_recommend_t computes): R = |Z(n)|,
 P = leading prefixes (a_1..a_L, phi <= n), Q = innermost runs (a_1..a_{L-1}), O = outer prefixes

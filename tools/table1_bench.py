@@ -58,11 +58,11 @@ def run(d, t, n):
 def main_csv():
     """--csv: the paper's Table 1 record (SPEC header dim,memo_dim,element,num_results,cpu_memo_us,
     par_memo_us,runtime_ms) with this build's GPU memo build as par_memo_us and memo + enumerate as runtime_ms;
-    cpu_memo_us is the single-thread CPU memo (Alg 2) recorded by `bench.py --study f4` (profiles/r02_f4_study.jsonl;
+    cpu_memo_us is the single-thread CPU memo (Alg 2) recorded by `bench.py --study f4` (profiles/r02x_f4_study.jsonl;
     blank when absent); the GPU enumerate time and factorizations/s are appended."""
     import json
-    cpu = {}   # recorded single-thread CPU memo times (bench.py --study f4, profiles/r02_f4_study.jsonl)
-    study = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02_f4_study.jsonl")
+    cpu = {}   # recorded single-thread CPU memo times (bench.py --study f4, profiles/r02x_f4_study.jsonl)
+    study = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02x_f4_study.jsonl")
     if os.path.exists(study):
         for line in open(study):
             r = json.loads(line)
