@@ -327,6 +327,13 @@ __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint4 lds128(uint32_t a)
 {
     uint4 v;
@@ -1728,12 +1735,14 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
     const uint32_t *__restrict__ cardT = wt.cardT;
     const uint64_t *__restrict__ offT = wt.offT;
     uint64_t acc_rows = 0, acc_hash = 0;
-    BlockInfo *bi = binfo[wib];
     // 32-bit shared address of this warp's block list, read back with ld.shared (keeps the compiler from
     // re-deriving the generic shared window -- S2R TID / CgaCtaId -- for every 32-row chunk)
     const uint64_t lane_k = (uint64_t)lane * kHashK;   // HASH: lane's share of the row-key multiply
     uint32_t bi_sa;   // (through a volatile move: the compiler keeps it in a register instead of recomputing it)
     asm volatile("mov.b32 %0, %1;" : "=r"(bi_sa) : "r"(smem_addr(binfo[wib])));
+    uint32_t ws_sa = 0;   // the word-stream staging buffer of this warp, the same way
+    if constexpr (kWordStream) asm volatile("mov.b32 %0, %1;" : "=r"(ws_sa) : "r"(smem_addr(wsb[wib])));
+    (void)ws_sa;
     const uint32_t cgq = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] / m : 0, cgr = (L >= 2) ? G.g[L >= 2 ? L - 2 : 0] % m : 0;
 
     (void)gw;
@@ -1981,10 +1990,12 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                 if (cc > 0) {
                     const int e = __popc(nz & ((1u << lane) - 1));
                     // byte address of the block's memo rows, pre-offset by its first output row (u64 wrap)
-                    bi[e].memo_row = M16 ? (uint64_t)(uintptr_t)wt.memo16 + (mrow - excl) * (uint64_t)(2 * (T > 0 ? T : 1))
-                                         : (uint64_t)(uintptr_t)wt.memo + (mrow - excl) * (uint64_t)(4 * (T > 0 ? T : 1));
-                    bi[e].start = excl;
-                    bi[e].v = (uint32_t)vv;
+                    const uint64_t mr = M16 ? (uint64_t)(uintptr_t)wt.memo16 + (mrow - excl) * (uint64_t)(2 * (T > 0 ? T : 1))
+                                            : (uint64_t)(uintptr_t)wt.memo + (mrow - excl) * (uint64_t)(4 * (T > 0 ? T : 1));
+                    // {memo_row, start, v} as one 16-B store through the register-kept shared address
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(bi_sa + 16u * (uint32_t)e),
+                                 "r"((uint32_t)mr), "r"((uint32_t)(mr >> 32)), "r"(excl), "r"((uint32_t)vv)
+                                 : "memory");
                 }
                 __syncwarp();
                 // flattened copy: rows q0 + lane of the round, owner block via block-start bitmask.
@@ -2004,7 +2015,7 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                         const uint32_t nr = (use - q0 < 32u * UNR) ? use - q0 : 32u * UNR;
                         const uint64_t G0 = (outpos + q0) * (uint64_t)D;        // first word (shard-relative)
                         const uint32_t sft = (uint32_t)(((uintptr_t)(out + G0) >> 2) & 3);
-                        uint32_t *sb = wsb[wib] + sft;
+                        const uint32_t sb = ws_sa + 4u * sft;   // 32-bit shared address of the staged run
                         // WSG 32-row chunks have their memo loads in flight before their rows go to shared memory
                         constexpr int WSG = (FZ_WS_GROUP < UNR) ? FZ_WS_GROUP : UNR;
 #pragma unroll
@@ -2032,25 +2043,25 @@ k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
 #pragma unroll
                             for (int g = 0; g < WSG; ++g) {
                                 if (!okg[g]) continue;
-                                uint32_t *rw = sb + (32 * (u0 + g) + lane) * D;
+                                const uint32_t rw = sb + 4u * (uint32_t)((32 * (u0 + g) + lane) * D);
 #pragma unroll
-                                for (int j = 0; j < L - 1; ++j) rw[j] = a[j];
-                                rw[L - 1] = vv[g];
+                                for (int j = 0; j < L - 1; ++j) sts32(rw + 4u * j, a[j]);
+                                sts32(rw + 4u * (L - 1), vv[g]);
 #pragma unroll
-                                for (int j = 0; j < T; ++j) rw[L + j] = tw[g][j];
+                                for (int j = 0; j < T; ++j) sts32(rw + 4u * (L + j), tw[g][j]);
                             }
                         }
                         __syncwarp();
                         const uint32_t W = nr * D, head = ((4 - sft) & 3) < W ? ((4 - sft) & 3) : W;
                         const uint32_t nv = (W - head) >> 2, tail0 = head + 4 * nv;
                         uint32_t *og = out + G0;
-                        if ((uint32_t)lane < head) st_cs_u32(og + lane, sb[lane]);
+                        if ((uint32_t)lane < head) st_cs_u32(og + lane, lds32(sb + 4u * lane));
                         {   // lane l stores vectors l, l + 32, ..: pointers advance by 512 B (no per-store 64-bit index math)
-                            uint32_t sa = smem_addr(sb + head) + 16u * (uint32_t)lane;
+                            uint32_t sa = sb + 4u * head + 16u * (uint32_t)lane;
                             uint32_t *gp = og + head + 4 * lane;
                             for (uint32_t v = lane; v < nv; v += 32, sa += 512, gp += 128) st_cs_v4(gp, lds128(sa));
                         }
-                        if ((uint32_t)lane < W - tail0) st_cs_u32(og + tail0 + lane, sb[tail0 + lane]);
+                        if ((uint32_t)lane < W - tail0) st_cs_u32(og + tail0 + lane, lds32(sb + 4u * (tail0 + lane)));
                         __syncwarp();
                         continue;
                     }

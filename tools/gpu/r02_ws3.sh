@@ -1,6 +1,4 @@
-O=gpurun_out; T=${1:-r02j}
-timeout 300 python tools/quick_time.py T95 T94 T63 T74 T31 > $O/${T}_auto.log 2>&1
-FZ_WORD_STREAM=1 timeout 300 python tools/quick_time.py T95 T94 T63 T74 > $O/${T}_ws1.log 2>&1
-FZ_WORD_STREAM=0 timeout 300 python tools/quick_time.py T95 T94 T63 T74 > $O/${T}_ws0.log 2>&1
-timeout 300 python tools/fill_modes.py > $O/${T}_fill_modes.log 2>&1
-timeout 600 python -m pytest tests -m gpu -x -q > $O/${T}_tests.log 2>&1; echo "rc=$?" >> $O/${T}_tests.log
+O=gpurun_out
+T=r02ws3
+FZ_LIB_PATH=ab/libfz_ws3.so timeout 1500 python -m pytest tests -m gpu -q -x > $O/${T}_tests.log 2>&1; echo "rc=$?" >> $O/${T}_tests.log
+bash tools/gpu/ab.sh $T "T95 T94 T63 T74 T1 C2 C2h C3t3 C3t2" ab/libfz_cur.so ab/libfz_ws3.so
