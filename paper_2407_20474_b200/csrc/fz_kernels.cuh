@@ -1658,6 +1658,9 @@ __device__ uint4 g_slice_trace[1u << 20];
 #ifndef FZ_HASH_MINB
 #define FZ_HASH_MINB 4  // HASH walk, d <= 6: resident CTAs per SM the register budget is sized for
 #endif
+#ifndef FZ_WIDE_MINB
+#define FZ_WIDE_MINB 2  // MATERIALIZE / HASH walk, d > 6 without the word stream: resident CTAs per SM
+#endif
 #ifndef FZ_HASH_UNR
 #define FZ_HASH_UNR 2   // HASH / COUNT (L <= 2) walk: 32-row chunks in flight per warp
 #endif
@@ -1687,7 +1690,7 @@ struct WalkTables {
 
 
 template <int D, int T, int MODE, bool M16 = false, bool WS = false, bool CS = false>
-__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (MODE == FZ_HASH && D <= 6 ? FZ_HASH_MINB : (D <= 6 ? 4 : (WS ? 4 : 2)))))
+__global__ void __launch_bounds__(walk_threads<MODE>(), (MODE == FZ_COUNT ? 1 : (MODE == FZ_HASH && D <= 6 ? FZ_HASH_MINB : (D <= 6 ? 4 : (WS ? 4 : FZ_WIDE_MINB)))))
 k5_walk(Gens G, uint64_t n64, PlanHdr *hdr,
                                                          const uint64_t *__restrict__ Tb, uint64_t top, WalkTables wt,
                                                          uint32_t *out, uint64_t out_cap_rows, uint64_t row_base,
