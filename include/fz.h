@@ -174,17 +174,21 @@ fz_status fz_shard_rows(const fz_memo *m, uint64_t n, fz_mode mode, int nshards,
 fz_status fz_layout_shard_rows(const fz_layout *lay, uint64_t n, fz_mode mode, int nshards, uint64_t *row_begin,
                                uint64_t *rows);
 
-/* Device plan-workspace bytes (a fixed bound: 256-B header + 64 B per slice,
- * at most 32 x (resident warps) slices). */
+/* Device plan-workspace bytes: the 256-B plan header (accumulators, shard geometry, slice queue); K5 unranks
+ * its slices itself, so no slice table is stored. */
 fz_status fz_plan_workspace_bytes(const fz_memo *m, uint64_t *bytes);
 
 /* K4 planner (asynchronous, entirely on the device): read |Z(n)| (or the
- * leading-prefix count) from the device tables, cut shard `shard` of
- * `nshards`, cut it into bounded slices of equal rows (MATERIALIZE, HASH) or
- * equal leading prefixes (COUNT), and unrank each slice start to its leading
- * prefix (a_1..a_L) and offset in the memo block, from the S / W tables:
+ * leading-prefix count) from the device tables and cut shard `shard` of
+ * `nshards` -- equal rows (MATERIALIZE, HASH) or equal modelled cost (COUNT:
+ * the C tables' cost ranks of whole outer prefixes) -- and its geometry of K5
+ * slices: equal rows, or, for MATERIALIZE / HASH walks with short rounds, equal
+ * walk cost (one unit per row plus a weight per visited leading prefix;
+ * DESIGN.md §6), or COUNT cost ranks in guided sizes.  K5 unranks each slice
+ * start to its leading prefix (a_1..a_L) and offset in the memo block from the
+ * S / W (/ C) tables:
  *   rank(a_1..a_L) = sum_j S_j[ r_{j-1} - (a_j + 1) g_j ],  r_j = n - sum_{i<=j} a_i g_i.
- * Writes the slice table and zeroes the result accumulators in d_plan
+ * Writes the plan header and zeroes the result accumulators in d_plan
  * (>= fz_plan_workspace_bytes, 256-B aligned, caller-owned) and returns a host
  * handle (free with fz_plan_free; the memo must outlive it).
  * Errors: FZ_EINVAL (n >= top, shard range, COUNT-only memo used for rows),
