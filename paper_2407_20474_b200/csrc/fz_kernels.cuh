@@ -2231,11 +2231,10 @@ __device__ __forceinline__ uint32_t add_prefix(const uint4 &w, uint32_t t, uint3
 {
     uint64_t lo, hi;
     const uint32_t tl = U8 ? (t < 8 ? t : 8) : t, th = (U8 && t > 8) ? t - 8 : 0;
-    asm("shl.b64 %0, %1, %2;" : "=l"(lo) : "l"(~0ull), "r"(8 * tl));   // PTX clamps shifts >= 64 to 0
-    lo = ~lo & 0x0101010101010101ull;
+    // bytes 0..tl-1 of 0x0101.. by one right shift (PTX clamps shifts >= 64 to 0: th = 0 gives no bytes)
+    asm("shr.b64 %0, %1, %2;" : "=l"(lo) : "l"(0x0101010101010101ull), "r"(64u - 8u * tl));
     if constexpr (U8) {
-        asm("shl.b64 %0, %1, %2;" : "=l"(hi) : "l"(~0ull), "r"(8 * th));
-        hi = ~hi & 0x0101010101010101ull;
+        asm("shr.b64 %0, %1, %2;" : "=l"(hi) : "l"(0x0101010101010101ull), "r"(64u - 8u * th));
         s = __dp4a(w.x, (uint32_t)lo, s);
         s = __dp4a(w.y, (uint32_t)(lo >> 32), s);
         s = __dp4a(w.z, (uint32_t)hi, s);
